@@ -1,0 +1,120 @@
+/*
+ * sbp.h -- C ABI of the B200 grid loopy-BP engine (libsbp.so).
+ *
+ * Plain pointers and sizes only; every device pointer is caller-owned
+ * (the library never allocates or frees caller memory) and every call is
+ * stream-ordered on the caller's `cudaStream_t` (passed as void*).
+ *
+ * Each entry point replaces one piece of the reference `sparsebp` grid
+ * engine (/root/reference/pkg/src/sparsebp):
+ *
+ *   sbp_init_msgs      <- bp.py:587-601      `_grid_store_init`
+ *   sbp_load_values    <- bp.py:488          values_in = unaries | log_unaries
+ *                                            (f64 host model -> padded f32 device)
+ *   sbp_iterate        <- bp.py:492-503 + numba_kernels.py:296-316,364-384
+ *                         (`_run_grid` -> `grid_pass_{sum,max}_{fast,standard,pruned}`);
+ *                         one SYNCHRONOUS iteration of all directed updates
+ *                         of a row range: _grid_h_* (:194-227) -> _fast_* /
+ *                         _std_* / _pruned_* (:35-101) -> _norm_*_store (:248-271)
+ *   sbp_beliefs        <- bp.py:711-744      `compute_beliefs`,
+ *                                            `compute_max_marginals`, `map_labels`
+ *   sbp_gather_store   <- bp.py:604-617      `_grid_store_to_messages`
+ *   sbp_max_abs_diff   <- bp.py:671-676      convergence test of `run_sweeps`
+ *
+ * Device layout:
+ *   values  [rows][W][Ms]          f32, labels >= M padded (0 sum / -inf max)
+ *   msgs    [4][rows+2][W][Ms]     f32; local row lr <-> global row r0+lr-1,
+ *                                  rows 0 and rows+1 are halo rows; slot k holds
+ *                                  the message INTO the node from direction k
+ *                                  (0 above, 1 left, 2 right, 3 below).
+ * Errors: every function returns SBP_OK or a negative code; the text of
+ * the last error of the calling thread is available from sbp_last_error().
+ * A message that cannot be normalised (reference DegenerateMessageError,
+ * bp.py:499-503) is reported through the device word `err`:
+ * min over failures of (iteration << 40 | reference directed-edge id).
+ */
+#ifndef SBP_H
+#define SBP_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SBP_API __attribute__((visibility("default")))
+#else
+#define SBP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBP_OK 0
+#define SBP_EINVAL (-1)
+#define SBP_ECUDA (-2)
+#define SBP_EUNSUPPORTED (-3)
+
+#define SBP_SUM 0
+#define SBP_MAX 1
+
+#define SBP_POT_BAND 0   /* Toeplitz band |x_i - x_j| <= R, weights in kernel params */
+#define SBP_POT_ELL 1    /* general per-column lists (ELL [m_max][Ms]) */
+#define SBP_POT_DENSE 2  /* dense O(M^2) comparison kernel (reference "standard") */
+
+#define SBP_MAX_R 32
+#define SBP_ERR_NONE 0xffffffffffffffffull
+
+typedef struct {
+    int H, W;      /* global grid */
+    int M, Ms;     /* labels and padded per-node stride (multiple of 4) */
+    int r0, rows;  /* this strip: global rows r0 .. r0+rows-1 */
+} sbp_grid;
+
+typedef struct {
+    int kind;            /* SBP_POT_* */
+    int domain;          /* SBP_SUM | SBP_MAX */
+    int floor_term;      /* 1: reference "fast" (fbar branch), 0: "pruned" */
+    int R;               /* BAND: radius, weights for d = x_i - x_j in [-R, R] */
+    int m_max;           /* ELL: entries per column */
+    float fbar[2];       /* per orientation: fbar (sum) or ln fbar (max) */
+    float band_w[2][2 * SBP_MAX_R + 1];   /* BAND: w[o][d + R] (residual | log value) */
+    const int32_t *ell_idx[2];            /* ELL: device [m_max][Ms], x_i per (k, x_j) */
+    const float *ell_w[2];                /* ELL: device [m_max][Ms] */
+    const float *dense_t[2];              /* DENSE: device [Ms][Ms], t[x_j][x_i] */
+} sbp_potential;
+
+SBP_API int sbp_version(void);
+SBP_API const char *sbp_last_error(void);
+
+/* Padded label stride the band kernels use for M labels (>= M, multiple of 4). */
+SBP_API int sbp_padded_labels(int M);
+
+SBP_API int sbp_init_msgs(const sbp_grid *g, int domain, float *msgs, void *stream);
+
+/* f64 [rows][W][M] (device) -> padded f32 values [rows][W][Ms]. */
+SBP_API int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream);
+
+/* One synchronous iteration over local rows [lr_begin, lr_end) (1-based
+ * strip rows; a full grid is r0 = 0, rows = H, lr in [1, H+1)). */
+SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                int iteration, unsigned long long *err, void *stream);
+
+/* Per-node beliefs (sum: normalised product, max: max-normalised scores),
+ * normalisers Z (sum only, f64) and argmax labels (lowest index on ties).
+ * Any of beliefs / normalizers / labels may be NULL.  bad_node receives
+ * min node id whose belief mass is zero (sum), untouched otherwise. */
+SBP_API int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float *msgs,
+                float *beliefs, double *normalizers, int32_t *labels,
+                unsigned long long *bad_node, void *stream);
+
+/* (2E, M) f32 store in reference directed-edge order (full grid only). */
+SBP_API int sbp_gather_store(const sbp_grid *g, const float *msgs, float *out, void *stream);
+
+/* max |a - b| over the real rows of two message buffers -> *out (device f32). */
+SBP_API int sbp_max_abs_diff(const sbp_grid *g, const float *a, const float *b, float *out,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBP_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of libsbp.so (the C ABI in include/sbp.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or ``make -C
+paper_1010_0012_b200/csrc``).  There is no fallback: if the shared object is
+missing or cannot be loaded, importing the engine raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libsbp.so"
+
+SBP_OK, SBP_EINVAL, SBP_ECUDA, SBP_EUNSUPPORTED = 0, -1, -2, -3
+SBP_SUM, SBP_MAX = 0, 1
+SBP_POT_BAND, SBP_POT_ELL, SBP_POT_DENSE = 0, 1, 2
+SBP_MAX_R = 32
+SBP_ERR_NONE = 0xFFFFFFFFFFFFFFFF
+
+
+class SbpGrid(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("M", ctypes.c_int),
+                ("Ms", ctypes.c_int), ("r0", ctypes.c_int), ("rows", ctypes.c_int)]
+
+
+class SbpPotential(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("domain", ctypes.c_int), ("floor_term", ctypes.c_int),
+                ("R", ctypes.c_int), ("m_max", ctypes.c_int),
+                ("fbar", ctypes.c_float * 2),
+                ("band_w", (ctypes.c_float * (2 * SBP_MAX_R + 1)) * 2),
+                ("ell_idx", ctypes.c_void_p * 2), ("ell_w", ctypes.c_void_p * 2),
+                ("dense_t", ctypes.c_void_p * 2)]
+
+
+class SbpError(RuntimeError):
+    """A libsbp call failed (bad arguments, unsupported shape or CUDA error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libsbp error {code}: {msg}")
+        self.code = code
+
+
+class UnsupportedByKernel(SbpError):
+    pass
+
+
+_lib = None
+
+# (name, restype, argtypes) -- mirrors include/sbp.h
+_P = ctypes.c_void_p
+_i = ctypes.c_int
+_PROTOS = {
+    "sbp_version": (_i, []),
+    "sbp_last_error": (ctypes.c_char_p, []),
+    "sbp_padded_labels": (_i, [_i]),
+    "sbp_init_msgs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P]),
+    "sbp_load_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P]),
+    "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
+                         _i, _i, _i, _P, _P]),
+    "sbp_beliefs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P, _P, _P, _P, _P]),
+    "sbp_gather_store": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P]),
+    "sbp_max_abs_diff": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P, _P]),
+}
+
+
+def lib():
+    """Load libsbp.so once; raises if it is absent (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        handle = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in _PROTOS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != SBP_OK:
+        msg = lib().sbp_last_error().decode(errors="replace")
+        if rc == SBP_EUNSUPPORTED:
+            raise UnsupportedByKernel(rc, msg)
+        raise SbpError(rc, msg)
+
+
+def exported_symbols() -> list[str]:
+    return list(_PROTOS)

@@ -1,0 +1,33 @@
+#pragma once
+#include "sbp_common.cuh"
+
+namespace sbp {
+
+cudaError_t launch_init_msgs(float *msgs, int H, int W, int M, int Ms, int r0, int rows,
+                             int domain, cudaStream_t s);
+cudaError_t launch_load_values(const double *src, float *dst, long long nodes, int M, int Ms,
+                               int domain, cudaStream_t s);
+cudaError_t launch_beliefs(int domain, const float *values, const float *msgs, int W, int M,
+                           int Ms, int rows, float *beliefs, double *normalizers, int *labels,
+                           unsigned long long *bad_node, cudaStream_t s);
+cudaError_t launch_gather_store(const float *msgs, int H, int W, int M, int Ms, float *out,
+                                cudaStream_t s);
+cudaError_t launch_max_abs_diff(const float *a, const float *b, int W, int M, int Ms, int rows,
+                                float *out, cudaStream_t s);
+
+struct EllArgs {
+    const float *values;
+    const float *msgs_in;
+    float *msgs_out;
+    unsigned long long *err;
+    long long slot_stride;
+    int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term, m_max;
+    float fbar[2];
+    const int *idx[2];
+    const float *w[2];
+};
+cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s);
+
+
+
+}  // namespace sbp

@@ -1,0 +1,293 @@
+// Fused synchronous banded BP iteration (sm_100a).
+//
+// One launch performs every directed message update of a row range for one
+// synchronous iteration.  Per node it reads the unary and the four incoming
+// messages ONCE (256-bit loads, label-contiguous [slot][row][W][Ms] layout),
+// forms the four exclusion products h_{i\j} in registers, and for each
+// outgoing direction computes the reference "fast" update
+//     sum:  out[x_j] = fbar * sum_x h(x) + sum_{d=-R..R} res(d) h(x_j + d)
+//     max:  out[x_j] = max(fbar + max_x h(x), max_d (val(d) + h(x_j + d)))
+// (numba_kernels.py:44-54 / 77-90, Eq. 7 / Eq. 11 of the paper) followed by
+// the reference normalisation (numba_kernels.py:248-271) and a 256-bit store
+// into the neighbour's incoming slot.
+//
+// Thread mapping: LP lanes own one node (pixel), each lane VL consecutive
+// labels (VL*LP = Ms).  Sums/maxima over labels are in-lane then xor
+// butterflies across the LP lanes (identical in every lane); the band's
+// out-of-lane neighbours h(x +- s) come from __shfl_up/down of the owning
+// lane.  The band is streamed in ascending x_i so every output accumulates its
+// terms in the reference's order (ascending x_i over the stored column).
+// Band weights depend only on d = x_i - x_j (Toeplitz potentials such as the
+// truncated linear / quadratic families); they are kernel parameters, so
+// every FFMA reads its weight straight from the constant bank.
+#pragma once
+
+#include "sbp_common.cuh"
+
+namespace sbp {
+
+struct BandArgs {
+    const float *values;   // [rows][W][Ms]
+    const float *msgs_in;  // [4][rows+2][W][Ms]
+    float *msgs_out;
+    unsigned long long *err;
+    long long slot_stride;  // (rows+2)*W*Ms
+    int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term;
+    float fbar[2];
+    float w[2][2 * SBP_MAX_R + 1];
+};
+
+template <int N>
+struct Vec8Loader {
+    static __device__ __forceinline__ void load(float (&dst)[N], const float *src) {
+#pragma unroll
+        for (int c = 0; c < N / 8; ++c) {
+            const float *p = src + 8 * c;
+            asm volatile(
+                "ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=f"(dst[8 * c + 0]), "=f"(dst[8 * c + 1]), "=f"(dst[8 * c + 2]),
+                  "=f"(dst[8 * c + 3]), "=f"(dst[8 * c + 4]), "=f"(dst[8 * c + 5]),
+                  "=f"(dst[8 * c + 6]), "=f"(dst[8 * c + 7])
+                : "l"(p));
+        }
+    }
+    static __device__ __forceinline__ void store(float *dst, const float (&v)[N]) {
+#pragma unroll
+        for (int c = 0; c < N / 8; ++c) {
+            float *p = dst + 8 * c;
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+                         "f"(v[8 * c + 0]), "f"(v[8 * c + 1]), "f"(v[8 * c + 2]),
+                         "f"(v[8 * c + 3]), "f"(v[8 * c + 4]), "f"(v[8 * c + 5]),
+                         "f"(v[8 * c + 6]), "f"(v[8 * c + 7])
+                         : "memory");
+        }
+    }
+};
+
+template <int LP>
+__device__ __forceinline__ float lanes_sum(float v) {
+#pragma unroll
+    for (int off = 1; off < LP; off <<= 1) v += __shfl_xor_sync(SBP_FULL_MASK, v, off);
+    return v;
+}
+
+template <int LP>
+__device__ __forceinline__ float lanes_max(float v) {
+#pragma unroll
+    for (int off = 1; off < LP; off <<= 1) v = fmaxf(v, __shfl_xor_sync(SBP_FULL_MASK, v, off));
+    return v;
+}
+
+// h value at lane-relative label offset t (t in [-R, VL+R)).
+template <int DOM, int VL, int LP, int R>
+__device__ __forceinline__ float band_h(const float (&h)[VL], int t, int j) {
+    constexpr float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    if (t >= 0 && t < VL) return h[t];
+    if (t < 0) {
+        const int s = -t;
+        const int q = (s + VL - 1) / VL;
+        if (q >= LP) return PAD;
+        const int idx = q * VL - s;
+        float v = __shfl_up_sync(SBP_FULL_MASK, h[idx], q, LP);
+        return j >= q ? v : PAD;
+    }
+    const int s = t - VL + 1;
+    const int q = (s + VL - 1) / VL;
+    if (q >= LP) return PAD;
+    const int idx = s - 1 - (q - 1) * VL;
+    float v = __shfl_down_sync(SBP_FULL_MASK, h[idx], q, LP);
+    return j + q < LP ? v : PAD;
+}
+
+// One outgoing direction: fast update + normalisation + store.
+template <int DOM, int VL, int LP, int R, int DIR>
+__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int j,
+                                               int x0, bool active, long long node_l,
+                                               long long r, int c) {
+    constexpr int O = dir_orient(DIR);
+    float out[VL];
+    if (DOM == SBP_SUM) {
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < VL; ++i) s += h[i];
+        s = lanes_sum<LP>(s);
+        const float base = a.floor_term ? a.fbar[O] * s : 0.0f;
+#pragma unroll
+        for (int i = 0; i < VL; ++i) out[i] = base;
+    } else {
+        float mx = h[0];
+#pragma unroll
+        for (int i = 1; i < VL; ++i) mx = fmaxf(mx, h[i]);
+        mx = lanes_max<LP>(mx);
+        const float base = a.floor_term ? a.fbar[O] + mx : -__builtin_huge_valf();
+#pragma unroll
+        for (int i = 0; i < VL; ++i) out[i] = base;
+    }
+    // Band, streamed in ascending x_i: term (x_i = x0+t) reaches out[i] at d = t - i.
+#pragma unroll
+    for (int t = -R; t < VL + R; ++t) {
+        const float hv = band_h<DOM, VL, LP, R>(h, t, j);
+#pragma unroll
+        for (int i = 0; i < VL; ++i) {
+            const int d = t - i;
+            if (d < -R || d > R) continue;
+            if (DOM == SBP_SUM) out[i] = fmaf(a.w[O][d + R], hv, out[i]);
+            else out[i] = fmaxf(out[i], a.w[O][d + R] + hv);
+        }
+    }
+    // Normalise (numba_kernels.py:248-271); padded labels stay 0 / -inf.
+    bool ok;
+    if (DOM == SBP_SUM) {
+        if (a.M < a.Ms) {
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                if (x0 + i >= a.M) out[i] = 0.0f;
+        }
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < VL; ++i) s += out[i];
+        s = lanes_sum<LP>(s);
+        ok = (s > 0.0f) && !isinf(s);
+        const float inv = __frcp_rn(s);
+#pragma unroll
+        for (int i = 0; i < VL; ++i) out[i] *= inv;
+    } else {
+        if (a.M < a.Ms) {
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                if (x0 + i >= a.M) out[i] = -__builtin_huge_valf();
+        }
+        float mx = out[0];
+#pragma unroll
+        for (int i = 1; i < VL; ++i) mx = fmaxf(mx, out[i]);
+        mx = lanes_max<LP>(mx);
+        ok = isfinite(mx);
+#pragma unroll
+        for (int i = 0; i < VL; ++i) out[i] -= mx;
+    }
+    if (!active) return;
+    const long long W = a.W;
+    const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
+    float *dst = a.msgs_out + dir_wslot(DIR) * a.slot_stride + (node_l + step) * a.Ms + x0;
+    Vec8Loader<VL>::store(dst, out);
+    if (!ok && j == 0) report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, DIR));
+}
+
+template <int DOM, int VL, int LP, int R>
+__global__ void __launch_bounds__(128) band_iter_kernel(const __grid_constant__ BandArgs a) {
+    constexpr int PPW = 32 / LP;
+    const int lane = threadIdx.x & 31;
+    const int j = lane % LP;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    if (warp * PPW >= npix) return;  // warp-uniform
+    long long p = warp * PPW + lane / LP;
+    const bool valid = p < npix;
+    if (!valid) p = npix - 1;
+    const int lr = a.lr_begin + (int)(p / a.W);
+    const int c = (int)(p % a.W);
+    const long long r = (long long)a.r0 + lr - 1;
+    const long long node_l = (long long)lr * a.W + c;
+    const int x0 = j * VL;
+
+    float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
+    Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
+    const float *mi = a.msgs_in + node_l * a.Ms + x0;
+    Vec8Loader<VL>::load(m0, mi);
+    Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+    Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+    Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+
+    const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
+    // Exclusion products in the reference order: unary, then slots 0..3
+    // ascending, skipping the excluded one (numba_kernels.py:194-227).
+    float ab[VL], h[VL];
+    if (DOM == SBP_SUM) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i) ab[i] = g[i] * m0[i];                  // g m0
+    } else {
+#pragma unroll
+        for (int i = 0; i < VL; ++i) ab[i] = g[i] + m0[i];
+    }
+    // send up (excl slot 0): ((g m1) m2) m3  -- consumes g first
+    if (__any_sync(SBP_FULL_MASK, valid && has_u)) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i)
+            h[i] = DOM == SBP_SUM ? ((g[i] * m1[i]) * m2[i]) * m3[i]
+                                  : ((g[i] + m1[i]) + m2[i]) + m3[i];
+        emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
+    }
+    // send left (excl slot 1): ((g m0) m2) m3
+    if (__any_sync(SBP_FULL_MASK, valid && has_l)) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i)
+            h[i] = DOM == SBP_SUM ? (ab[i] * m2[i]) * m3[i] : (ab[i] + m2[i]) + m3[i];
+        emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
+    }
+#pragma unroll
+    for (int i = 0; i < VL; ++i) ab[i] = DOM == SBP_SUM ? ab[i] * m1[i] : ab[i] + m1[i];  // g m0 m1
+    // send right (excl slot 2): ((g m0) m1) m3
+    if (__any_sync(SBP_FULL_MASK, valid && has_r)) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i) h[i] = DOM == SBP_SUM ? ab[i] * m3[i] : ab[i] + m3[i];
+        emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
+    }
+    // send down (excl slot 3): ((g m0) m1) m2
+    if (__any_sync(SBP_FULL_MASK, valid && has_d)) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i) h[i] = DOM == SBP_SUM ? ab[i] * m2[i] : ab[i] + m2[i];
+        emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+    }
+}
+
+}  // namespace sbp
+
+namespace sbp {
+
+using BandLaunchFn = cudaError_t (*)(const BandArgs &, cudaStream_t);
+
+template <int DOM, int VL, int LP, int R>
+cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
+    constexpr int PPW = 32 / LP;
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long warps = (npix + PPW - 1) / PPW;
+    const long long blocks = (warps + 3) / 4;
+    if (blocks <= 0) return cudaSuccess;
+    band_iter_kernel<DOM, VL, LP, R><<<(unsigned)blocks, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Band radii with a compiled kernel; a potential of radius r runs on the
+// smallest listed R >= r (extra taps carry weight 0 / -inf: exact no-ops).
+#define SBP_BAND_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
+
+template <int MS, int DOM, int VL>
+BandLaunchFn pick_band_r(int R) {
+    if constexpr (VL > MS) {
+        return nullptr;
+    } else {
+        switch (R) {
+#define SBP_CASE(RR)                                                      \
+    case RR:                                                              \
+        if constexpr (RR < MS) return &launch_band<DOM, VL, MS / VL, RR>; \
+        else return nullptr;
+            SBP_BAND_RADII(SBP_CASE)
+#undef SBP_CASE
+        default: return nullptr;
+        }
+    }
+}
+
+template <int MS>
+BandLaunchFn pick_band(int dom, int vl, int R) {
+    if (dom == SBP_SUM) {
+        if (vl == 8) return pick_band_r<MS, SBP_SUM, 8>(R);
+        if (vl == 16) return pick_band_r<MS, SBP_SUM, 16>(R);
+    } else {
+        if (vl == 8) return pick_band_r<MS, SBP_MAX, 8>(R);
+        if (vl == 16) return pick_band_r<MS, SBP_MAX, 16>(R);
+    }
+    return nullptr;
+}
+
+}  // namespace sbp

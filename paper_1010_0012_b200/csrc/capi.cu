@@ -1,0 +1,187 @@
+// extern "C" entry points of libsbp.so (declared in include/sbp.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "aux_kernels.cuh"
+#include "band_kernel.cuh"
+
+namespace sbp {
+template <int MS>
+BandLaunchFn pick_band(int dom, int vl, int R);
+}
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+    if (e == cudaSuccess) return SBP_OK;
+    return fail(SBP_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+int check_grid(const sbp_grid *g) {
+    if (!g) return fail(SBP_EINVAL, "grid is NULL");
+    if (g->H < 1 || g->W < 1 || g->M < 1) return fail(SBP_EINVAL, "bad grid %dx%d M=%d", g->H, g->W, g->M);
+    if (g->Ms < g->M || g->Ms % 8) return fail(SBP_EINVAL, "bad padded stride Ms=%d for M=%d", g->Ms, g->M);
+    if (g->Ms > 256) return fail(SBP_EUNSUPPORTED, "M=%d > 256 labels is not supported", g->M);
+    if (g->rows < 1 || g->r0 < 0 || g->r0 + g->rows > g->H)
+        return fail(SBP_EINVAL, "bad strip r0=%d rows=%d of H=%d", g->r0, g->rows, g->H);
+    return SBP_OK;
+}
+
+const int kRadii[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32};
+
+int band_vl(int Ms) {
+    if (const char *e = getenv("SBP_BAND_VL")) {
+        int v = atoi(e);
+        if ((v == 8 || v == 16) && v <= Ms) return v;
+    }
+    return Ms >= 128 ? 16 : 8;
+}
+
+sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R) {
+    switch (Ms) {
+    case 8: return sbp::pick_band<8>(dom, vl, R);
+    case 16: return sbp::pick_band<16>(dom, vl, R);
+    case 32: return sbp::pick_band<32>(dom, vl, R);
+    case 64: return sbp::pick_band<64>(dom, vl, R);
+    case 128: return sbp::pick_band<128>(dom, vl, R);
+    case 256: return sbp::pick_band<256>(dom, vl, R);
+    default: return nullptr;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbp_version(void) { return 1; }
+
+const char *sbp_last_error(void) { return g_err; }
+
+int sbp_padded_labels(int M) {
+    if (M < 1) return fail(SBP_EINVAL, "M must be >= 1");
+    int ms = 8;
+    while (ms < M && ms < 256) ms <<= 1;
+    if (ms < M) ms = (M + 7) / 8 * 8;
+    return ms;
+}
+
+int sbp_init_msgs(const sbp_grid *g, int domain, float *msgs, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!msgs) return fail(SBP_EINVAL, "msgs is NULL");
+    return cuda_status(sbp::launch_init_msgs(msgs, g->H, g->W, g->M, g->Ms, g->r0, g->rows,
+                                             domain, (cudaStream_t)stream),
+                       "sbp_init_msgs");
+}
+
+int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!src || !dst) return fail(SBP_EINVAL, "NULL pointer");
+    return cuda_status(sbp::launch_load_values(src, dst, (long long)g->rows * g->W, g->M, g->Ms,
+                                               domain, (cudaStream_t)stream),
+                       "sbp_load_values");
+}
+
+int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                const float *msgs_in, float *msgs_out, int lr_begin, int lr_end, int iteration,
+                unsigned long long *err, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!pot || !values || !msgs_in || !msgs_out || !err) return fail(SBP_EINVAL, "NULL pointer");
+    if (pot->domain != SBP_SUM && pot->domain != SBP_MAX) return fail(SBP_EINVAL, "bad domain");
+    if (lr_begin < 1 || lr_end > g->rows + 1 || lr_begin > lr_end)
+        return fail(SBP_EINVAL, "bad row range [%d, %d) of %d rows", lr_begin, lr_end, g->rows);
+    if (lr_begin == lr_end) return SBP_OK;
+    if (iteration < 0 || iteration >= (1 << 23)) return fail(SBP_EINVAL, "bad iteration index");
+    const long long slot = (long long)(g->rows + 2) * g->W * g->Ms;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (pot->kind == SBP_POT_BAND) {
+        if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
+        int Rk = 0;
+        for (int r : kRadii)
+            if (r >= pot->R && r < g->Ms) { Rk = r; break; }
+        const int vl = band_vl(g->Ms);
+        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk) : nullptr;
+        if (!fn)
+            return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
+        sbp::BandArgs a;
+        a.values = values;
+        a.msgs_in = msgs_in;
+        a.msgs_out = msgs_out;
+        a.err = err;
+        a.slot_stride = slot;
+        a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
+        a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
+        a.floor_term = pot->floor_term;
+        const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+        for (int o = 0; o < 2; ++o) {
+            a.fbar[o] = pot->fbar[o];
+            for (int k = 0; k < 2 * SBP_MAX_R + 1; ++k) a.w[o][k] = pad;
+            for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
+        }
+        return cuda_status(fn(a, s), "sbp_iterate(band)");
+    }
+    if (pot->kind == SBP_POT_ELL || pot->kind == SBP_POT_DENSE) {
+        if (pot->m_max < 0 || !pot->ell_idx[0] || !pot->ell_idx[1] || !pot->ell_w[0] ||
+            !pot->ell_w[1])
+            return fail(SBP_EINVAL, "ELL potential arrays missing");
+        sbp::EllArgs a;
+        a.values = values;
+        a.msgs_in = msgs_in;
+        a.msgs_out = msgs_out;
+        a.err = err;
+        a.slot_stride = slot;
+        a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
+        a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
+        a.floor_term = pot->kind == SBP_POT_DENSE ? 0 : pot->floor_term;
+        a.m_max = pot->m_max;
+        for (int o = 0; o < 2; ++o) {
+            a.fbar[o] = pot->fbar[o];
+            a.idx[o] = pot->ell_idx[o];
+            a.w[o] = pot->ell_w[o];
+        }
+        return cuda_status(sbp::launch_ell(pot->domain, a, s), "sbp_iterate(ell)");
+    }
+    return fail(SBP_EINVAL, "unknown potential kind %d", pot->kind);
+}
+
+int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float *msgs,
+                float *beliefs, double *normalizers, int32_t *labels,
+                unsigned long long *bad_node, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!values || !msgs) return fail(SBP_EINVAL, "NULL pointer");
+    return cuda_status(sbp::launch_beliefs(domain, values, msgs, g->W, g->M, g->Ms, g->rows,
+                                           beliefs, normalizers, labels, bad_node,
+                                           (cudaStream_t)stream),
+                       "sbp_beliefs");
+}
+
+int sbp_gather_store(const sbp_grid *g, const float *msgs, float *out, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "gather needs the full grid");
+    if (!msgs || !out) return fail(SBP_EINVAL, "NULL pointer");
+    return cuda_status(sbp::launch_gather_store(msgs, g->H, g->W, g->M, g->Ms, out,
+                                                (cudaStream_t)stream),
+                       "sbp_gather_store");
+}
+
+int sbp_max_abs_diff(const sbp_grid *g, const float *a, const float *b, float *out,
+                     void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!a || !b || !out) return fail(SBP_EINVAL, "NULL pointer");
+    return cuda_status(sbp::launch_max_abs_diff(a, b, g->W, g->M, g->Ms, g->rows, out,
+                                                (cudaStream_t)stream),
+                       "sbp_max_abs_diff");
+}
+
+}  // extern "C"

@@ -1,0 +1,512 @@
+"""GPU grid BP engine and the reference-shaped public API.
+
+Drop-in surface of the reference ``sparsebp`` grid path (bp.py:620-744):
+
+* ``run_sweeps(model, n_sweeps, kernel="fast", domain="sum", schedule=...,
+  convergence_tol=None) -> MessageStore``
+* ``compute_beliefs(model, store) -> BeliefTable``
+* ``compute_max_marginals(model, store) -> ndarray (N, M)``
+* ``map_labels(scores | BeliefTable | MessageStore) -> ndarray (N,) int64``
+
+with the reference's exception types and attributes
+(``DegenerateMessageError.edge``, ``DegenerateBeliefError.node``,
+``UnsafePotentialError``) and validation (bp.py:411-433).
+
+Schedule: the GPU runs the SYNCHRONOUS (Jacobi) schedule -- all directed
+messages of iteration t+1 from those of iteration t.  The reference's
+default is its canonical in-place sequential sweep (bp.py:630-633), which
+gives different numbers, so ``schedule`` must be passed
+explicitly as ``"synchronous"``; the default raises instead of silently
+changing semantics.
+
+Every device computation goes through libsbp.so (hand-written sm_100a
+kernels, ``csrc/``); torch provides device memory, streams and events only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .plan import PotentialPlan, plan_potential
+
+__all__ = ["SYNCHRONOUS", "DegenerateMessageError", "DegenerateBeliefError",
+           "UnsafePotentialError", "SweepStats", "BeliefTable", "MessageStore", "GridEngine",
+           "run_sweeps", "compute_beliefs", "compute_max_marginals", "map_labels"]
+
+SYNCHRONOUS = "synchronous"
+KERNELS = ("standard", "fast", "pruned")
+DOMAINS = ("sum", "max")
+
+
+class DegenerateMessageError(ValueError):
+    """A message could not be normalised (reference bp.py:58-67)."""
+
+    def __init__(self, msg: str, edge: tuple[int, int] | None = None):
+        super().__init__(msg)
+        self.edge = edge
+
+
+class DegenerateBeliefError(ValueError):
+    """A belief vector is zero everywhere (reference bp.py:70-75)."""
+
+    def __init__(self, msg: str, node: int | None = None):
+        super().__init__(msg)
+        self.node = node
+
+
+class UnsafePotentialError(ValueError):
+    """Fast max-sum requires every stored value >= the floor (bp.py:78-79)."""
+
+
+@dataclass
+class SweepStats:
+    """Reference bp.py:95-107; ``sweep_seconds`` are device times per iteration."""
+
+    sweep_seconds: list = field(default_factory=list)
+    madds: int = 0
+    n_updates: int = 0
+    sweeps_run: int = 0
+    converged: bool = False
+
+    @property
+    def seconds_per_sweep(self) -> float:
+        return sum(self.sweep_seconds) / max(len(self.sweep_seconds), 1)
+
+
+@dataclass
+class BeliefTable:
+    """Reference bp.py:174-187 (beliefs sum to 1 per node, Z_i normalisers)."""
+
+    beliefs: np.ndarray
+    normalizers: np.ndarray
+    labels: np.ndarray | None = None   # argmax computed on the device
+
+
+# ---------------------------------------------------------------------------
+# model introspection (reference MrfModel or this package's GridMrf)
+# ---------------------------------------------------------------------------
+
+def _shared_potential(model):
+    pot = getattr(model, "shared_potential", None)
+    if pot is not None:
+        return pot
+    pots = model.potentials
+    if len(pots) == 0:
+        return None
+    first = pots[0]
+    if any(p is not first for p in pots):
+        raise NotImplementedError(
+            "GPU grid engine needs one potential shared by all edges (reference grid-engine "
+            "precondition, bp.py:652-654); per-edge potentials are not supported")
+    return first
+
+
+def _validate(model, kernel: str, domain: str, pot) -> None:
+    """Reference ``_validate_run_args`` (bp.py:411-433) on the shared potential."""
+    if kernel not in KERNELS:
+        raise ValueError(f"kernel must be one of {KERNELS}, got {kernel!r}")
+    if domain not in DOMAINS:
+        raise ValueError(f"domain must be one of {DOMAINS}, got {domain!r}")
+    if pot is None:
+        return
+    sparse = hasattr(pot, "col_indptr")
+    if kernel in ("fast", "pruned") and not sparse:
+        raise TypeError(f"kernel={kernel!r} requires SparseTruncatedPotential on every edge, "
+                        f"found {type(pot).__name__}")
+    if domain == "sum":
+        if sparse:
+            if pot.fbar < 0 or (np.asarray(pot.col_values) < 0).any():
+                raise ValueError("sum-product potentials must be nonnegative (fbar >= 0)")
+        elif (np.asarray(pot.table) < 0).any():
+            raise ValueError("sum-product potentials must be nonnegative")
+    if domain == "max" and kernel == "fast":
+        lp = pot.to_log()
+        if hasattr(lp, "maxsum_safe") and not lp.maxsum_safe:
+            raise UnsafePotentialError(
+                "fast max-sum requires values >= fbar on every edge potential")
+
+
+def _edge_endpoints(H: int, W: int, d: int) -> tuple[int, int]:
+    """Reference directed-edge id -> (i, j) (bp.py:154-156 over mrf.py:401-411)."""
+    e = d // 2
+    r = min(e // (2 * W - 1), H - 1)
+    o = e - r * (2 * W - 1)
+    if r < H - 1:
+        if o < 2 * (W - 1):
+            c, horiz = o // 2, o % 2 == 0
+        else:
+            c, horiz = W - 1, False
+    else:
+        c, horiz = o, True
+    a = r * W + c
+    b = a + (1 if horiz else W)
+    return (a, b) if d % 2 == 0 else (b, a)
+
+
+def _stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class GridEngine:
+    """Device state of one grid (or one row strip of it) for one domain.
+
+    Owns the padded f32 value table, two message buffers (ping-pong) and
+    the error word; the potential plan's arrays live on the device too.
+    """
+
+    def __init__(self, model, domain: str = "sum", kernel: str = "fast", device=None,
+                 r0: int = 0, rows: int | None = None, values: np.ndarray | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("the GPU grid engine needs a CUDA device (no CPU fallback)")
+        self.lib = L.lib()
+        self.model = model
+        if model.grid_shape is None:
+            raise NotImplementedError("GPU engine supports grid models only (grid_shape is None)")
+        self.H, self.W = (int(v) for v in model.grid_shape)
+        self.M = int(model.M)
+        self.domain = domain
+        self.kernel = kernel
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        pot = _shared_potential(model)
+        _validate(model, kernel, domain, pot)
+        self.r0 = r0
+        self.rows = self.H - r0 if rows is None else rows
+        self.Ms = self.lib.sbp_padded_labels(self.M)
+        if self.Ms > 256:
+            raise NotImplementedError(f"M={self.M} > 256 labels is not supported on the GPU path")
+        self.grid = L.SbpGrid(self.H, self.W, self.M, self.Ms, self.r0, self.rows)
+        self.dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
+        self.plan: PotentialPlan | None = None
+        if pot is not None:
+            self.plan = plan_potential(pot, domain, kernel, self.M, self.Ms)
+            self._pot_struct = self._make_pot_struct(self.plan)
+        with torch.cuda.device(self.device):
+            shape = (4, self.rows + 2, self.W, self.Ms)
+            self.msgs = [torch.empty(shape, dtype=torch.float32, device=self.device),
+                         torch.empty(shape, dtype=torch.float32, device=self.device)]
+            self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
+            self.values = torch.empty((self.rows, self.W, self.Ms), dtype=torch.float32,
+                                      device=self.device)
+            self.upload_values(values)
+        self.cur = 0
+        self.iterations = 0
+        self.reset()
+
+    # -- setup -------------------------------------------------------------
+    def _make_pot_struct(self, plan: PotentialPlan) -> L.SbpPotential:
+        s = L.SbpPotential()
+        s.kind, s.domain, s.floor_term = plan.kind, self.dom, plan.floor_term
+        s.R, s.m_max = plan.R, plan.m_max
+        s.fbar[0], s.fbar[1] = plan.fbar
+        if plan.kind == L.SBP_POT_BAND:
+            for o in range(2):
+                for k, v in enumerate(plan.band_w[o]):
+                    s.band_w[o][k] = float(v)
+        else:
+            idx = torch.from_numpy(np.ascontiguousarray(plan.ell_idx)).to(self.device)
+            w = torch.from_numpy(np.ascontiguousarray(plan.ell_w, dtype=np.float32)).to(self.device)
+            plan.device_arrays = [idx, w]
+            for o in range(2):
+                s.ell_idx[o] = idx[o].data_ptr()
+                s.ell_w[o] = w[o].data_ptr()
+        return s
+
+    def upload_values(self, values: np.ndarray | torch.Tensor | None = None) -> None:
+        """Host f64 unaries (sum) / log unaries (max) -> padded f32 device table."""
+        if values is None:
+            src = self.model.unaries if self.domain == "sum" else self.model.log_unaries
+            values = src[self.r0 * self.W:(self.r0 + self.rows) * self.W]
+        if isinstance(values, torch.Tensor):
+            dev = values.to(self.device, dtype=torch.float64)
+        else:
+            host = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64))
+            dev = host.to(self.device, non_blocking=host.is_pinned())
+        L.check(self.lib.sbp_load_values(ctypes_ref(self.grid), self.dom, _ptr(dev),
+                                         _ptr(self.values), _stream_handle()))
+        self._staging = dev   # keep alive until the stream consumed it
+
+    def reset(self) -> None:
+        for buf in self.msgs:
+            L.check(self.lib.sbp_init_msgs(ctypes_ref(self.grid), self.dom, _ptr(buf),
+                                           _stream_handle()))
+        self.err.fill_(-1)
+        self.cur = 0
+        self.iterations = 0
+
+    # -- iteration ---------------------------------------------------------
+    @property
+    def current(self) -> torch.Tensor:
+        return self.msgs[self.cur]
+
+    def iterate_rows(self, lr_begin: int, lr_end: int, stream: int | None = None) -> None:
+        """One synchronous iteration over local rows [lr_begin, lr_end) from the
+        current buffer into the other one (does not flip buffers)."""
+        if self.plan is None:
+            return
+        L.check(self.lib.sbp_iterate(
+            ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
+            _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), lr_begin, lr_end,
+            self.iterations, _ptr(self.err), _stream_handle() if stream is None else stream))
+
+    def flip(self) -> None:
+        self.cur = 1 - self.cur
+        self.iterations += 1
+
+    def step(self, n: int = 1, events: list | None = None) -> None:
+        for _ in range(n):
+            if events is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+            self.iterate_rows(1, self.rows + 1)
+            self.flip()
+            if events is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record()
+                events.append((ev0, ev1))
+
+    def max_abs_delta(self) -> float:
+        out = torch.zeros(1, dtype=torch.float32, device=self.device)
+        L.check(self.lib.sbp_max_abs_diff(ctypes_ref(self.grid), _ptr(self.msgs[0]),
+                                          _ptr(self.msgs[1]), _ptr(out), _stream_handle()))
+        return float(out.item())
+
+    def error(self) -> tuple[int, int] | None:
+        """(iteration, directed edge id) of the first degenerate message, or None."""
+        key = int(self.err.item()) & 0xFFFFFFFFFFFFFFFF
+        if key == L.SBP_ERR_NONE:
+            return None
+        return key >> 40, key & ((1 << 40) - 1)
+
+    def raise_if_degenerate(self) -> None:
+        e = self.error()
+        if e is not None:
+            it, d = e
+            i, j = _edge_endpoints(self.H, self.W, d)
+            raise DegenerateMessageError(
+                f"degenerate message on edge {i}->{j} (synchronous iteration {it})", edge=(i, j))
+
+    # -- read-out ----------------------------------------------------------
+    def beliefs_device(self, want_beliefs: bool = True, want_labels: bool = True):
+        n = self.rows * self.W
+        b = (torch.empty((n, self.M), dtype=torch.float32, device=self.device)
+             if want_beliefs else None)
+        z = (torch.empty(n, dtype=torch.float64, device=self.device)
+             if want_beliefs and self.domain == "sum" else None)
+        lab = torch.empty(n, dtype=torch.int32, device=self.device) if want_labels else None
+        bad = torch.full((1,), -1, dtype=torch.int64, device=self.device)
+        L.check(self.lib.sbp_beliefs(
+            ctypes_ref(self.grid), self.dom, _ptr(self.values), _ptr(self.current),
+            _ptr(b) if b is not None else None, _ptr(z) if z is not None else None,
+            _ptr(lab) if lab is not None else None, _ptr(bad), _stream_handle()))
+        return b, z, lab, bad
+
+    def labels(self) -> torch.Tensor:
+        _, _, lab, bad = self.beliefs_device(want_beliefs=False)
+        self._check_bad(bad)
+        return lab
+
+    def _check_bad(self, bad: torch.Tensor) -> None:
+        if self.domain != "sum":
+            return
+        v = int(bad.item()) & 0xFFFFFFFFFFFFFFFF
+        if v != L.SBP_ERR_NONE:
+            node = v + self.r0 * self.W
+            raise DegenerateBeliefError(f"belief of node {node} is zero everywhere", node=node)
+
+    def store_device(self) -> torch.Tensor:
+        """(2E, M) f32 messages in reference directed-edge order."""
+        E = self.H * (self.W - 1) + self.W * (self.H - 1)
+        out = torch.empty((2 * E, self.M), dtype=torch.float32, device=self.device)
+        L.check(self.lib.sbp_gather_store(ctypes_ref(self.grid), _ptr(self.current), _ptr(out),
+                                          _stream_handle()))
+        return out
+
+    def msgs4(self) -> np.ndarray:
+        """Reference-layout (4, N, M) f64 copy of the current messages."""
+        cur = self.current[:, 1:self.rows + 1, :, :self.M]
+        return cur.reshape(4, self.rows * self.W, self.M).double().cpu().numpy()
+
+
+def ctypes_ref(obj):
+    import ctypes
+    return ctypes.byref(obj)
+
+
+class MessageStore:
+    """Result of ``run_sweeps`` (reference bp.py:110-171).
+
+    ``data`` -- the (2E, M) f64 array in directed-edge order -- is
+    materialised lazily from the device (a gather kernel + one copy), since
+    at 2048x1536 with M=128 it is 12.9 GB of host memory.
+    """
+
+    def __init__(self, model, domain: str, engine: GridEngine | None = None,
+                 data: np.ndarray | None = None):
+        if domain not in DOMAINS:
+            raise ValueError(f"domain must be one of {DOMAINS}, got {domain!r}")
+        self.model = model
+        self.domain = domain
+        self.engine = engine
+        self._data = data
+        self.stats: SweepStats | None = None
+
+    @property
+    def n_directed(self) -> int:
+        return 2 * int(self.model.n_edges)
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._data is None:
+            if self.engine is None or self.engine.plan is None:
+                fill = 1.0 / self.model.M if self.domain == "sum" else 0.0
+                self._data = np.full((self.n_directed, self.model.M), fill, dtype=np.float64)
+            else:
+                self._data = self.engine.store_device().double().cpu().numpy()
+        return self._data
+
+    def edge_id(self, i: int, j: int) -> int:
+        H, W = self.model.grid_shape
+        ri, ci = divmod(int(i), W)
+        d = int(j) - int(i)
+        if d == 1 and ci + 1 < W:
+            e = ri * (2 * W - 1) + (2 * ci if ri < H - 1 else ci)
+            return 2 * e
+        if d == -1 and ci > 0:
+            return self.edge_id(j, i) + 1
+        if d == W and ri + 1 < H:
+            e = ri * (2 * W - 1) + 2 * ci + (1 if ci + 1 < W else 0)
+            return 2 * e
+        if d == -W and ri > 0:
+            return self.edge_id(j, i) + 1
+        raise KeyError(f"no directed edge {i}->{j} in model")
+
+    def vector(self, i: int, j: int) -> np.ndarray:
+        return self.data[self.edge_id(i, j)]
+
+    def endpoints(self, d: int) -> tuple[int, int]:
+        H, W = self.model.grid_shape
+        return _edge_endpoints(H, W, int(d))
+
+    def check_normalized(self, atol: float = 1e-6) -> None:
+        """Domain invariant (bp.py:162-171) at fp32 tolerance."""
+        if self.n_directed == 0:
+            return
+        if self.domain == "sum":
+            sums = self.data.sum(axis=1)
+            assert np.abs(sums - 1.0).max() <= atol, "sum-domain message does not sum to 1"
+            assert (self.data >= 0).all(), "sum-domain message has negative entries"
+        else:
+            assert (self.data.max(axis=1) == 0.0).all(), "max-domain message max is not exactly 0"
+
+
+def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
+               schedule=None, convergence_tol: float | None = None, device=None,
+               engine: GridEngine | None = None) -> MessageStore:
+    """Run ``n_sweeps`` synchronous iterations on the GPU (reference bp.py:620-703).
+
+    One synchronous iteration updates every directed edge once, like one
+    reference sweep, but from the previous iteration's messages only.
+    """
+    if schedule is None:
+        raise NotImplementedError(
+            "the GPU engine runs the synchronous (Jacobi) schedule; the reference default is "
+            "its sequential in-place sweep, which gives different messages. Pass "
+            "schedule='synchronous' to opt in.")
+    if schedule != SYNCHRONOUS:
+        raise NotImplementedError(f"unsupported schedule {schedule!r}; use 'synchronous'")
+    if n_sweeps < 0:
+        raise ValueError(f"n_sweeps must be >= 0, got {n_sweeps}")
+    pot = _shared_potential(model) if model.n_edges else None
+    _validate(model, kernel, domain, pot)
+    stats = SweepStats()
+    if model.n_edges == 0 or n_sweeps == 0:
+        store = MessageStore(model, domain, engine=None)
+        store.stats = stats
+        return store
+    eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device)
+    if engine is not None:
+        eng.reset()
+    per_iter = 2 * int(model.n_edges)
+    events: list = []
+    for _ in range(n_sweeps):
+        eng.step(1, events=events)
+        stats.sweeps_run += 1
+        stats.n_updates += per_iter
+        if convergence_tol is not None:
+            if eng.max_abs_delta() < convergence_tol:
+                stats.converged = True
+                break
+    torch.cuda.synchronize(eng.device)
+    stats.sweep_seconds = [a.elapsed_time(b) / 1e3 for a, b in events]
+    stats.madds = eng.plan.madds_per_update * stats.n_updates
+    eng.raise_if_degenerate()
+    store = MessageStore(model, domain, engine=eng)
+    store.stats = stats
+    return store
+
+
+def _engine_of(store) -> GridEngine | None:
+    return getattr(store, "engine", None)
+
+
+def compute_beliefs(model, msgs: MessageStore) -> BeliefTable:
+    """Normalised beliefs b_i = g_i * prod incoming / Z_i (bp.py:711-725)."""
+    if msgs.domain != "sum":
+        raise ValueError("compute_beliefs requires sum-product messages")
+    eng = _engine_of(msgs)
+    if eng is None or eng.plan is None:
+        u = np.asarray(model.unaries, dtype=np.float64)
+        if model.n_edges:
+            raise TypeError("compute_beliefs needs a store produced by this engine")
+        z = u.sum(axis=1)
+        if not (z > 0).all():
+            node = int(np.flatnonzero(~(z > 0))[0])
+            raise DegenerateBeliefError(f"belief of node {node} is zero everywhere", node=node)
+        return BeliefTable(u / z[:, None], z, labels=np.argmax(u / z[:, None], axis=1))
+    b, z, lab, bad = eng.beliefs_device()
+    eng._check_bad(bad)
+    return BeliefTable(b.double().cpu().numpy(), z.cpu().numpy(),
+                       labels=lab.long().cpu().numpy())
+
+
+def compute_max_marginals(model, msgs: MessageStore) -> np.ndarray:
+    """log g + sum of incoming messages, minus the row max (bp.py:728-738)."""
+    if msgs.domain != "max":
+        raise ValueError("compute_max_marginals requires max-sum messages")
+    eng = _engine_of(msgs)
+    if eng is None or eng.plan is None:
+        lu = np.asarray(model.log_unaries, dtype=np.float64)
+        if model.n_edges:
+            raise TypeError("compute_max_marginals needs a store produced by this engine")
+        return lu - lu.max(axis=1, keepdims=True)
+    b, _, _, _ = eng.beliefs_device(want_labels=False)
+    return b.double().cpu().numpy()
+
+
+def map_labels(scores) -> np.ndarray:
+    """Per-node argmax, lowest index on ties (bp.py:741-744).
+
+    Accepts a BeliefTable, a score array, or -- as an extension -- a
+    MessageStore from this engine, in which case only the labels leave the
+    device.
+    """
+    if isinstance(scores, MessageStore):
+        eng = _engine_of(scores)
+        if eng is not None and eng.plan is not None:
+            return eng.labels().cpu().numpy().astype(np.int64)
+        arr = (compute_beliefs(scores.model, scores).beliefs if scores.domain == "sum"
+               else compute_max_marginals(scores.model, scores))
+        return np.argmax(arr, axis=1)
+    if isinstance(scores, BeliefTable):
+        if scores.labels is not None:
+            return scores.labels
+        return np.argmax(scores.beliefs, axis=1)
+    return np.argmax(np.asarray(scores), axis=1)

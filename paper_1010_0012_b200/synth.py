@@ -149,3 +149,28 @@ def build_config_model(cfg: StereoConfig, seed: int = 0, height: int | None = No
     left, right, _ = noisy_stereo_pair(H, W, cfg.M, cfg.sigma, seed)
     unaries, log_unaries = stereo_unary_field(left, right, cfg.M, cfg.beta, cfg.T_u)
     return GridMrf(H, W, cfg.M, unaries, cfg.build_potential(), log_unaries=log_unaries)
+
+
+def config_values(cfg: StereoConfig, domain: str, seed: int = 0, r0: int = 0,
+                  rows: int | None = None) -> np.ndarray:
+    """(rows*W, M) f64 unaries (sum) or analytic log unaries (max) of a row
+    range.  A pixel's unary depends only on its own image row, so a strip
+    is computed without the rest of the grid."""
+    rows = cfg.height - r0 if rows is None else rows
+    left, right, _ = noisy_stereo_pair(cfg.height, cfg.width, cfg.M, cfg.sigma, seed)
+    u, lu = stereo_unary_field(left[r0:r0 + rows], right[r0:r0 + rows], cfg.M, cfg.beta, cfg.T_u)
+    return u if domain == "sum" else lu
+
+
+class StripModel:
+    """Minimal model view for one strip of a config grid: geometry and the
+    shared potential, no full-grid unary table (the engine takes the strip's
+    values explicitly)."""
+
+    def __init__(self, cfg: StereoConfig):
+        self.M = cfg.M
+        self.grid_shape = (cfg.height, cfg.width)
+        self.shared_potential = cfg.build_potential()
+        H, W = cfg.height, cfg.width
+        self.n_edges = H * (W - 1) + W * (H - 1)
+        self.n_nodes = H * W

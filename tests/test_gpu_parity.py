@@ -1,0 +1,237 @@
+"""GPU parity: the sm_100a path (through libsbp.so) against the f64 oracle.
+
+Tolerances (north_star: fp32 beliefs/messages within 1e-5 relative, MAP
+labels identical except at exact ties):
+* sum-product messages and beliefs: reference ``rel_deviation``
+  (cli.py:35-40) <= 1e-5 over entries >= 1e-30 (fp32 cannot hold the f64
+  tail below that);
+* max-sum messages / scores (log domain): |gpu - ref| <= 1e-5 * max(1, |ref|);
+* labels: equal wherever the f64 top-2 gap exceeds the fp32 tie band
+  (sum: 1e-5 relative to the node's largest belief; max: 1e-4 absolute).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import paper_1010_0012_b200 as sbp  # noqa: E402
+from golden_util import GOLDEN, load_case, manifest  # noqa: E402
+from paper_1010_0012_b200 import synth  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+MAN = manifest()
+SUM_TOL = 1e-5
+MAX_TOL = 1e-5
+SYNC = "synchronous"
+
+
+def max_dev(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    both_inf = np.isneginf(a) & np.isneginf(b)
+    d = np.where(both_inf, 0.0, np.abs(a - b) / np.maximum(1.0, np.abs(b)))
+    return float(d.max()) if d.size else 0.0
+
+
+def assert_labels(gpu_labels, ref_scores, domain):
+    ref_labels = np.argmax(ref_scores, axis=1)
+    gap = oracle.top2_gap(ref_scores)
+    if domain == "sum":
+        decided = gap > 1e-5 * ref_scores.max(axis=1)
+    else:
+        decided = gap > 1e-4
+    bad = (gpu_labels != ref_labels) & decided
+    assert not bad.any(), f"{bad.sum()} decided labels differ (of {decided.sum()})"
+    return int((~decided).sum())
+
+
+def check_run(model, iters, domain, kernel="fast", ref_msgs4=None):
+    """Run GPU + oracle (unless given) and compare store, beliefs, labels."""
+    if ref_msgs4 is None:
+        ref_msgs4 = oracle.sync_run(model, iters, domain, kernel)
+    store = sbp.run_sweeps(model, iters, kernel=kernel, domain=domain, schedule=SYNC)
+    ref_store = oracle.store_data(model, ref_msgs4)
+    if domain == "sum":
+        assert oracle.rel_deviation(store.data, ref_store, floor=1e-30) <= SUM_TOL
+        bt = sbp.compute_beliefs(model, store)
+        rb, rz = oracle.beliefs(model, ref_msgs4)
+        assert oracle.rel_deviation(bt.beliefs, rb, floor=1e-30) <= SUM_TOL
+        assert oracle.rel_deviation(bt.normalizers, rz) <= 1e-4
+        assert_labels(sbp.map_labels(bt), rb, "sum")
+        np.testing.assert_array_equal(sbp.map_labels(store), sbp.map_labels(bt))
+    else:
+        assert max_dev(store.data, ref_store) <= MAX_TOL
+        s = sbp.compute_max_marginals(model, store)
+        rs = oracle.max_marginals(model, ref_msgs4)
+        assert max_dev(s, rs) <= MAX_TOL
+        assert_labels(sbp.map_labels(s), rs, "max")
+        assert (store.data.max(axis=1) == 0.0).all()
+    return store
+
+
+SMALL = sorted(n for n, e in MAN["cases"].items() if e["kind"] == "sync" and "degenerate" not in e
+               and (GOLDEN / f"{n}.npz").exists()
+               and "msgs4" in np.load(GOLDEN / f"{n}.npz").files)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_golden_small_cases(name):
+    e = MAN["cases"][name]
+    model, z = load_case(name)
+    if model.n_edges == 0:
+        pytest.skip("no edges")
+    check_run(model, e["iters"], e["domain"], e["kernel"], ref_msgs4=z["msgs4"])
+
+
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_c1(domain):
+    model = synth.build_config_model(synth.CONFIGS["C1"])
+    check_run(model, 10, domain)
+
+
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_c2(domain):
+    model = synth.build_config_model(synth.CONFIGS["C2"])
+    check_run(model, 50, domain)
+
+
+def test_c3_reduced_grid():
+    cfg = synth.CONFIGS["C3"]
+    model = synth.build_config_model(cfg, height=96, width=128)
+    check_run(model, 100, "max")
+
+
+@pytest.mark.parametrize("T", [2, 5, 9, 17, 33])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_c5_reduced_grid(T, domain):
+    model = synth.build_config_model(synth.CONFIGS[f"C5_T{T}"], height=24, width=40)
+    check_run(model, 20, domain)
+
+
+def test_c4_reduced_grid():
+    model = synth.build_config_model(synth.CONFIGS["C4"], height=48, width=160)
+    check_run(model, 100, "sum")
+
+
+@pytest.mark.parametrize("kernel", ["standard", "pruned"])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_other_kernels_c1(kernel, domain):
+    model = synth.build_config_model(synth.CONFIGS["C1"], height=24, width=32)
+    check_run(model, 10, domain, kernel)
+
+
+def test_fast_equals_standard_max_bitwise():
+    """Reference claim (bp.py:325-333): fast max-sum == standard bitwise."""
+    model = synth.build_config_model(synth.CONFIGS["C2"], height=40, width=56)
+    a = sbp.run_sweeps(model, 15, kernel="fast", domain="max", schedule=SYNC).data
+    b = sbp.run_sweeps(model, 15, kernel="standard", domain="max", schedule=SYNC).data
+    np.testing.assert_array_equal(a, b)
+
+
+def test_deterministic_and_store_layout():
+    model = synth.build_config_model(synth.CONFIGS["C2"], height=64, width=96)
+    s1 = sbp.run_sweeps(model, 7, schedule=SYNC)
+    s2 = sbp.run_sweeps(model, 7, schedule=SYNC)
+    np.testing.assert_array_equal(s1.data, s2.data)
+    # gather order == reference _grid_store_to_messages over the msgs4 layout
+    np.testing.assert_array_equal(s1.data, oracle.store_data(model, s1.engine.msgs4()))
+    s1.check_normalized(atol=1e-5)
+
+
+def test_degenerate_message_raises_with_edge():
+    e = MAN["cases"]["sync_degenerate_sum"]
+    model, _ = load_case("sync_degenerate_sum")
+    with pytest.raises(sbp.DegenerateMessageError) as ei:
+        sbp.run_sweeps(model, e["iters"], schedule=SYNC)
+    ids = e["degenerate"]["directed_edge_ids"]
+    store = sbp.MessageStore(model, "sum")
+    assert store.edge_id(*ei.value.edge) == min(ids)
+
+
+@pytest.mark.parametrize("name", sorted(n for n, e in MAN["cases"].items() if e["kind"] == "exact"))
+def test_chain_exact_marginals(name):
+    model, z = load_case(name)
+    W = model.grid_shape[1]
+    bt = sbp.compute_beliefs(model, sbp.run_sweeps(model, W + 1, schedule=SYNC))
+    assert oracle.rel_deviation(bt.beliefs, z["marginals"]) <= SUM_TOL
+    if MAN["cases"][name]["map_unique"]:
+        s = sbp.compute_max_marginals(model, sbp.run_sweeps(model, W + 1, domain="max",
+                                                            schedule=SYNC))
+        np.testing.assert_array_equal(sbp.map_labels(s), z["map_config"])
+
+
+def test_convergence_tol_matches_oracle():
+    model = synth.build_config_model(synth.CONFIGS["C1"], height=16, width=20)
+    tol = 1e-3
+    _, st = oracle.sync_run(model, 200, "sum", "fast", convergence_tol=tol, return_stats=True)
+    store = sbp.run_sweeps(model, 200, schedule=SYNC, convergence_tol=tol)
+    assert store.stats.converged and st["converged"]
+    assert abs(store.stats.sweeps_run - st["iterations"]) <= 1
+
+
+def test_row_strips_with_halo_exchange_bitwise():
+    """Two strips (the multi-GPU decomposition) on one device, halo rows
+    copied between them each iteration, equal the whole-grid run bitwise."""
+    from paper_1010_0012_b200.strips import StripRunner
+    model = synth.build_config_model(synth.CONFIGS["C2"], height=37, width=50)
+    full = sbp.run_sweeps(model, 9, schedule=SYNC).engine.msgs4()
+    for n_strips in (2, 3):
+        runner = StripRunner.local(model, n_strips, "sum", "fast")
+        runner.run(9)
+        np.testing.assert_array_equal(runner.gather_msgs4(), full)
+
+
+@pytest.mark.slow
+def test_c4_full_size_light_cone():
+    """Full 2048x1536, M=128: after t iterations a message depends only on the
+    t-neighbourhood, so crops of radius t+1 run by the oracle pin the full-size
+    GPU result at sampled nodes."""
+    cfg = synth.CONFIGS["C4"]
+    model = synth.build_config_model(cfg)
+    t = 6
+    store = sbp.run_sweeps(model, t, schedule=SYNC)
+    gpu = store.engine
+    H, W = model.grid_shape
+    rng = np.random.default_rng(1)
+    pts = [(0, 0), (H - 1, W - 1), (H // 2, W // 2)] + \
+        [(int(rng.integers(0, H)), int(rng.integers(0, W))) for _ in range(3)]
+    cur = gpu.current
+    for (r, c) in pts:
+        r0, r1 = max(0, r - t - 1), min(H, r + t + 2)
+        c0, c1 = max(0, c - t - 1), min(W, c + t + 2)
+        # crop borders that are real grid borders stay borders; interior crop
+        # edges are > t away from (r, c), so they cannot influence it yet
+        idx = (np.arange(r0, r1)[:, None] * W + np.arange(c0, c1)[None, :]).ravel()
+        crop = sbp.GridMrf(r1 - r0, c1 - c0, model.M, model.unaries[idx], model.shared_potential,
+                           log_unaries=model.log_unaries[idx])
+        ref = oracle.sync_run(crop, t, "sum", "fast")
+        n_crop = (r - r0) * (c1 - c0) + (c - c0)
+        got = cur[:, r + 1, c, :model.M].double().cpu().numpy()
+        assert oracle.rel_deviation(got, ref[:, n_crop], floor=1e-30) <= SUM_TOL
+
+
+@pytest.mark.slow
+def test_c4_full_size_invariants():
+    model = synth.build_config_model(synth.CONFIGS["C4"])
+    eng = sbp.GridEngine(model, "sum", "fast")
+    eng.step(100)
+    torch.cuda.synchronize()
+    eng.raise_if_degenerate()
+    cur = eng.current[:, 1:-1, :, :model.M]
+    sums = cur.sum(dim=-1)
+    H, W = model.grid_shape
+    # real slots sum to 1; ghost slots stay exactly 1 per entry
+    real = torch.ones_like(sums, dtype=torch.bool)
+    real[0, 0, :] = False
+    real[1, :, 0] = False
+    real[2, :, W - 1] = False
+    real[3, H - 1, :] = False
+    assert (sums[real] - 1).abs().max().item() < 1e-5
+    assert (cur[~real] == 1).all()
+    lab = eng.labels()
+    assert lab.shape == (H * W,) and int(lab.min()) >= 0 and int(lab.max()) < model.M
