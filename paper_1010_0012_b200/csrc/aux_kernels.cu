@@ -33,15 +33,30 @@ __global__ void init_msgs_kernel(float *msgs, int H, int W, int M, int Ms, int r
     }
 }
 
+// f64 model values -> padded f32 device table, one warp per node.  In the
+// max domain each node's log unary is shifted by its own maximum (computed
+// and subtracted in f64): every message is max-normalised and the
+// max-marginals subtract the row max, so a per-node constant changes no
+// result, but it keeps the magnitudes entering the fp32 h sums small.
 __global__ void load_values_kernel(const double *src, float *dst, long long nodes, int M, int Ms,
                                    int domain) {
-    const long long total = nodes * Ms;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long n = i / Ms;
-        const int x = (int)(i % Ms);
-        dst[i] = x < M ? (float)src[n * M + x]
-                       : (domain == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+    const int lane = threadIdx.x & 31;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long n = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < nodes;
+         n += warps) {
+        const double *s = src + n * M;
+        double shift = 0.0;
+        if (domain == SBP_MAX) {
+            double mx = -__builtin_huge_val();
+            for (int x = lane; x < M; x += 32) mx = fmax(mx, s[x]);
+            for (int off = 16; off; off >>= 1)
+                mx = fmax(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
+            if (isfinite(mx)) shift = mx;
+        }
+        float *d = dst + n * Ms;
+        for (int x = lane; x < Ms; x += 32)
+            d[x] = x < M ? (float)(s[x] - shift)
+                         : (domain == SBP_SUM ? 0.0f : -__builtin_huge_valf());
     }
 }
 
@@ -85,11 +100,17 @@ __global__ void beliefs_kernel(const float *values, const float *msgs, int W, in
                 }
                 for (int off = 16; off; off >>= 1)
                     mx = fmaxf(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
-                if (mx > 0.0f && (mx < 0x1p-60f || mx > 0x1p60f)) {
-                    const float inv = 1.0f / mx;
+                // rescale by an exact power of two so the running max stays
+                // in [1, 2): no rounding, no drift towards the denormals
+                if (mx > 0.0f) {
+                    int e;
+                    frexpf(mx, &e);
+                    e -= 1;
+                    if (e != 0) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) b[q] *= inv;
-                    scale *= (double)mx;
+                        for (int q = 0; q < 8; ++q) b[q] = ldexpf(b[q], -e);
+                        scale = ldexp(scale, e);
+                    }
                 }
             }
 #pragma unroll
@@ -110,27 +131,28 @@ __global__ void beliefs_kernel(const float *values, const float *msgs, int W, in
             }
             if (lane == 0 && normalizers) normalizers[n] = (double)z * scale;
         } else {
-            float s[8];
-            float mx = -__builtin_huge_valf();
+            // scores in f64: ln g + m0 + m1 + m2 + m3 - max, rounded once
+            double s[8];
+            double mx = -__builtin_huge_val();
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int x = lane + 32 * q;
                 if (x < M) {
-                    float v = g[x];
-                    for (int k = 0; k < 4; ++k) v += m[k * slot + x];
+                    double v = (double)g[x];
+                    for (int k = 0; k < 4; ++k) v += (double)m[k * slot + x];
                     s[q] = v;
-                    mx = fmaxf(mx, v);
+                    mx = fmax(mx, v);
                 } else {
-                    s[q] = -__builtin_huge_valf();
+                    s[q] = -__builtin_huge_val();
                 }
             }
             for (int off = 16; off; off >>= 1)
-                mx = fmaxf(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
+                mx = fmax(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int x = lane + 32 * q;
                 if (x < M) {
-                    const float v = s[q] - mx;
+                    const float v = (float)(s[q] - mx);
                     if (beliefs) beliefs[n * M + x] = v;
                     if (v > best) { best = v; best_x = x; }
                 }
@@ -216,7 +238,7 @@ cudaError_t launch_init_msgs(float *msgs, int H, int W, int M, int Ms, int r0, i
 
 cudaError_t launch_load_values(const double *src, float *dst, long long nodes, int M, int Ms,
                                int domain, cudaStream_t s) {
-    load_values_kernel<<<grid_for(nodes * Ms, 256), 256, 0, s>>>(src, dst, nodes, M, Ms, domain);
+    load_values_kernel<<<grid_for(nodes * 32, 256), 256, 0, s>>>(src, dst, nodes, M, Ms, domain);
     return cudaGetLastError();
 }
 

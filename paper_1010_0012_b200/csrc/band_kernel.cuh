@@ -99,6 +99,28 @@ __device__ __forceinline__ float band_h(const float (&h)[VL], int t, int j) {
     return j + q < LP ? v : PAD;
 }
 
+// Knuth TwoSum: a + b = s + e exactly (no FMA contraction: adds only).
+// Infinite sums (-inf log unaries / padding) carry e = 0.
+__device__ __forceinline__ void two_sum(float a, float b, float &s, float &e) {
+    s = a + b;
+    const float bp = s - a;
+    const float ee = (a - (s - bp)) + (b - bp);
+    e = isfinite(s) ? ee : 0.0f;
+}
+
+// h'[i] = (s[i] - c) + e[i] with c = max over the node's labels of s.
+template <int VL, int LP>
+__device__ __forceinline__ void shift_compensated(const float (&s)[VL], const float (&e)[VL],
+                                                  float (&h)[VL]) {
+    float c = s[0];
+#pragma unroll
+    for (int i = 1; i < VL; ++i) c = fmaxf(c, s[i]);
+    c = lanes_max<LP>(c);
+    if (!isfinite(c)) c = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VL; ++i) h[i] = (s[i] - c) + e[i];
+}
+
 // One outgoing direction: fast update + normalisation + store.
 template <int DOM, int VL, int LP, int R, int DIR>
 __device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int j,
@@ -199,44 +221,89 @@ __global__ void __launch_bounds__(128) band_iter_kernel(const __grid_constant__ 
     Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
 
     const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
-    // Exclusion products in the reference order: unary, then slots 0..3
-    // ascending, skipping the excluded one (numba_kernels.py:194-227).
-    float ab[VL], h[VL];
+    float h[VL];
     if (DOM == SBP_SUM) {
+        // Exclusion products in the reference order: unary, then slots 0..3
+        // ascending, skipping the excluded one (numba_kernels.py:194-227).
+        float ab[VL];
 #pragma unroll
         for (int i = 0; i < VL; ++i) ab[i] = g[i] * m0[i];                  // g m0
+        if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
+#pragma unroll
+            for (int i = 0; i < VL; ++i) h[i] = ((g[i] * m1[i]) * m2[i]) * m3[i];
+            emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
+        }
+        if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
+#pragma unroll
+            for (int i = 0; i < VL; ++i) h[i] = (ab[i] * m2[i]) * m3[i];
+            emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
+        }
+#pragma unroll
+        for (int i = 0; i < VL; ++i) ab[i] = ab[i] * m1[i];                 // g m0 m1
+        if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
+#pragma unroll
+            for (int i = 0; i < VL; ++i) h[i] = ab[i] * m3[i];
+            emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
+        }
+        if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
+#pragma unroll
+            for (int i = 0; i < VL; ++i) h[i] = ab[i] * m2[i];
+            emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+        }
     } else {
+        // Max-sum: h = ln g + sum of three messages.  Its entries can reach
+        // tens in magnitude while the normalised messages resolve ~1e-7, so
+        // fp32 rounding of the sum dominates the error (measured: 8.5e-6 on
+        // C5 T=9).  The sum is formed error-free (TwoSum: h = s + e exactly
+        // up to ~2^-48 relative), shifted by the node's max of s, and only
+        // then rounded: h' = (s - c) + e.  Messages are shift-invariant.
+        float sa[VL], ea[VL], s2[VL], e2[VL];
 #pragma unroll
-        for (int i = 0; i < VL; ++i) ab[i] = g[i] + m0[i];
-    }
-    // send up (excl slot 0): ((g m1) m2) m3  -- consumes g first
-    if (__any_sync(SBP_FULL_MASK, valid && has_u)) {
+        for (int i = 0; i < VL; ++i) two_sum(g[i], m0[i], sa[i], ea[i]);    // g + m0
+        if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
 #pragma unroll
-        for (int i = 0; i < VL; ++i)
-            h[i] = DOM == SBP_SUM ? ((g[i] * m1[i]) * m2[i]) * m3[i]
-                                  : ((g[i] + m1[i]) + m2[i]) + m3[i];
-        emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
-    }
-    // send left (excl slot 1): ((g m0) m2) m3
-    if (__any_sync(SBP_FULL_MASK, valid && has_l)) {
+            for (int i = 0; i < VL; ++i) {
+                float t, e;
+                two_sum(g[i], m1[i], s2[i], e2[i]);
+                two_sum(s2[i], m2[i], t, e); s2[i] = t; e2[i] += e;
+                two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
+            }
+            shift_compensated<VL, LP>(s2, e2, h);
+            emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
+        }
+        if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
 #pragma unroll
-        for (int i = 0; i < VL; ++i)
-            h[i] = DOM == SBP_SUM ? (ab[i] * m2[i]) * m3[i] : (ab[i] + m2[i]) + m3[i];
-        emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
-    }
+            for (int i = 0; i < VL; ++i) {
+                float t, e;
+                two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
+                two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
+            }
+            shift_compensated<VL, LP>(s2, e2, h);
+            emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
+        }
 #pragma unroll
-    for (int i = 0; i < VL; ++i) ab[i] = DOM == SBP_SUM ? ab[i] * m1[i] : ab[i] + m1[i];  // g m0 m1
-    // send right (excl slot 2): ((g m0) m1) m3
-    if (__any_sync(SBP_FULL_MASK, valid && has_r)) {
+        for (int i = 0; i < VL; ++i) {                                       // g + m0 + m1
+            float t, e;
+            two_sum(sa[i], m1[i], t, e); sa[i] = t; ea[i] += e;
+        }
+        if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
 #pragma unroll
-        for (int i = 0; i < VL; ++i) h[i] = DOM == SBP_SUM ? ab[i] * m3[i] : ab[i] + m3[i];
-        emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
-    }
-    // send down (excl slot 3): ((g m0) m1) m2
-    if (__any_sync(SBP_FULL_MASK, valid && has_d)) {
+            for (int i = 0; i < VL; ++i) {
+                float e;
+                two_sum(sa[i], m3[i], s2[i], e); e2[i] = ea[i] + e;
+            }
+            shift_compensated<VL, LP>(s2, e2, h);
+            emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
+        }
+        if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
 #pragma unroll
-        for (int i = 0; i < VL; ++i) h[i] = DOM == SBP_SUM ? ab[i] * m2[i] : ab[i] + m2[i];
-        emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+            for (int i = 0; i < VL; ++i) {
+                float e;
+                two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
+            }
+            shift_compensated<VL, LP>(s2, e2, h);
+            emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+        }
     }
 }
 

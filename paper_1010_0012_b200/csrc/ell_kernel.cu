@@ -8,6 +8,7 @@
 // conflict-light LDS; entries of a column are visited in ascending x_i, the
 // reference's order, padded entries carry weight 0 (sum) / -inf (max).
 #include "aux_kernels.cuh"
+#include "band_kernel.cuh"   // two_sum, shift_compensated, lanes_max
 
 namespace sbp {
 
@@ -109,15 +110,61 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
         for (int k = 0; k < 4; ++k) m[k][q] = in ? mp[k * a.slot_stride + x] : PAD;
     }
     float h[ELL_QMAX];
+    const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
+    if (DOM == SBP_SUM) {
 #define SBP_H(E0, E1, E2)                                                                  \
-    for (int q = 0; q < ELL_QMAX; ++q)                                                     \
-        h[q] = DOM == SBP_SUM ? ((g[q] * m[E0][q]) * m[E1][q]) * m[E2][q]                  \
-                              : ((g[q] + m[E0][q]) + m[E1][q]) + m[E2][q];
-    if (c + 1 < a.W) { SBP_H(0, 1, 3) ell_emit<DOM, 0>(a, h, hs, lane, true, node_l, r, c); }
-    if (c > 0) { SBP_H(0, 2, 3) ell_emit<DOM, 1>(a, h, hs, lane, true, node_l, r, c); }
-    if (r + 1 < a.H) { SBP_H(0, 1, 2) ell_emit<DOM, 2>(a, h, hs, lane, true, node_l, r, c); }
-    if (r > 0) { SBP_H(1, 2, 3) ell_emit<DOM, 3>(a, h, hs, lane, true, node_l, r, c); }
+    for (int q = 0; q < ELL_QMAX; ++q) h[q] = ((g[q] * m[E0][q]) * m[E1][q]) * m[E2][q];
+        if (has_u) { SBP_H(1, 2, 3) ell_emit<DOM, 3>(a, h, hs, lane, true, node_l, r, c); }
+        if (has_l) { SBP_H(0, 2, 3) ell_emit<DOM, 1>(a, h, hs, lane, true, node_l, r, c); }
+        if (has_r) { SBP_H(0, 1, 3) ell_emit<DOM, 0>(a, h, hs, lane, true, node_l, r, c); }
+        if (has_d) { SBP_H(0, 1, 2) ell_emit<DOM, 2>(a, h, hs, lane, true, node_l, r, c); }
 #undef SBP_H
+    } else {
+        // Same error-free (TwoSum) sums and shift as the band kernel, in the
+        // same operation order, so fast (band) and standard (dense) max-sum
+        // stay bit-identical as in the reference (bp.py:325-333).
+        float sa[ELL_QMAX], ea[ELL_QMAX], s2[ELL_QMAX], e2[ELL_QMAX];
+        for (int q = 0; q < ELL_QMAX; ++q) two_sum(g[q], m[0][q], sa[q], ea[q]);
+        if (has_u) {
+            for (int q = 0; q < ELL_QMAX; ++q) {
+                float t, e;
+                two_sum(g[q], m[1][q], s2[q], e2[q]);
+                two_sum(s2[q], m[2][q], t, e); s2[q] = t; e2[q] += e;
+                two_sum(s2[q], m[3][q], t, e); s2[q] = t; e2[q] += e;
+            }
+            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
+            ell_emit<DOM, 3>(a, h, hs, lane, true, node_l, r, c);
+        }
+        if (has_l) {
+            for (int q = 0; q < ELL_QMAX; ++q) {
+                float t, e;
+                two_sum(sa[q], m[2][q], s2[q], e); e2[q] = ea[q] + e;
+                two_sum(s2[q], m[3][q], t, e); s2[q] = t; e2[q] += e;
+            }
+            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
+            ell_emit<DOM, 1>(a, h, hs, lane, true, node_l, r, c);
+        }
+        for (int q = 0; q < ELL_QMAX; ++q) {
+            float t, e;
+            two_sum(sa[q], m[1][q], t, e); sa[q] = t; ea[q] += e;
+        }
+        if (has_r) {
+            for (int q = 0; q < ELL_QMAX; ++q) {
+                float e;
+                two_sum(sa[q], m[3][q], s2[q], e); e2[q] = ea[q] + e;
+            }
+            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
+            ell_emit<DOM, 0>(a, h, hs, lane, true, node_l, r, c);
+        }
+        if (has_d) {
+            for (int q = 0; q < ELL_QMAX; ++q) {
+                float e;
+                two_sum(sa[q], m[2][q], s2[q], e); e2[q] = ea[q] + e;
+            }
+            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
+            ell_emit<DOM, 2>(a, h, hs, lane, true, node_l, r, c);
+        }
+    }
 }
 
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s) {

@@ -25,6 +25,7 @@ kernels, ``csrc/``); torch provides device memory, streams and events only.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -227,7 +228,10 @@ class GridEngine:
         if isinstance(values, torch.Tensor):
             dev = values.to(self.device, dtype=torch.float64)
         else:
-            host = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64))
+            arr = np.ascontiguousarray(values, dtype=np.float64)
+            with warnings.catch_warnings():   # read-only model arrays: never written
+                warnings.simplefilter("ignore", UserWarning)
+                host = torch.from_numpy(arr)
             dev = host.to(self.device, non_blocking=host.is_pinned())
         L.check(self.lib.sbp_load_values(ctypes_ref(self.grid), self.dom, _ptr(dev),
                                          _ptr(self.values), _stream_handle()))
