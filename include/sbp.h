@@ -79,7 +79,8 @@ typedef struct {
     float band_w[2][2 * SBP_MAX_R + 1];   /* BAND: w[o][d + R] (residual | log value) */
     const int32_t *ell_idx[2];            /* ELL: device [m_max][Ms], x_i per (k, x_j) */
     const float *ell_w[2];                /* ELL: device [m_max][Ms] */
-    const float *dense_t[2];              /* DENSE: device [Ms][Ms], t[x_j][x_i] */
+    const float *dense_t[2];              /* reserved (DENSE currently runs on the ELL
+                                             arrays with m_max = M, idx[k][x] = k) */
 } sbp_potential;
 
 SBP_API int sbp_version(void);
@@ -88,16 +89,23 @@ SBP_API const char *sbp_last_error(void);
 /* Padded label stride the band kernels use for M labels (>= M, multiple of 4). */
 SBP_API int sbp_padded_labels(int M);
 
-SBP_API int sbp_init_msgs(const sbp_grid *g, int domain, float *msgs, void *stream);
+/* Initial messages (bp.py:587-601).  ghosts_only = 1 writes only the border
+ * (ghost) slots, which the iteration kernels never write: enough for a fresh
+ * buffer when the first iteration runs with SBP_ITER_FIRST. */
+SBP_API int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs,
+                          void *stream);
 
 /* f64 [rows][W][M] (device) -> padded f32 values [rows][W][Ms]. */
 SBP_API int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream);
 
 /* One synchronous iteration over local rows [lr_begin, lr_end) (1-based
- * strip rows; a full grid is r0 = 0, rows = H, lr in [1, H+1)). */
+ * strip rows; a full grid is r0 = 0, rows = H, lr in [1, H+1)).  With
+ * SBP_ITER_FIRST in flags the incoming messages are taken to be the
+ * reference initial messages and msgs_in is not read. */
+#define SBP_ITER_FIRST 1
 SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
-                const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
-                int iteration, unsigned long long *err, void *stream);
+                        const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                        int iteration, int flags, unsigned long long *err, void *stream);
 
 /* Per-node beliefs (sum: normalised product, max: max-normalised scores),
  * normalisers Z (sum only, f64) and argmax labels (lowest index on ties).

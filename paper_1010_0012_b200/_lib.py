@@ -17,6 +17,7 @@ SBP_SUM, SBP_MAX = 0, 1
 SBP_POT_BAND, SBP_POT_ELL, SBP_POT_DENSE = 0, 1, 2
 SBP_MAX_R = 32
 SBP_ERR_NONE = 0xFFFFFFFFFFFFFFFF
+SBP_ITER_FIRST = 1
 
 
 class SbpGrid(ctypes.Structure):
@@ -54,10 +55,10 @@ _PROTOS = {
     "sbp_version": (_i, []),
     "sbp_last_error": (ctypes.c_char_p, []),
     "sbp_padded_labels": (_i, [_i]),
-    "sbp_init_msgs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P]),
+    "sbp_init_msgs": (_i, [ctypes.POINTER(SbpGrid), _i, _i, _P, _P]),
     "sbp_load_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P]),
     "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
-                         _i, _i, _i, _P, _P]),
+                         _i, _i, _i, _i, _P, _P]),
     "sbp_beliefs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P, _P, _P, _P, _P]),
     "sbp_gather_store": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P]),
     "sbp_max_abs_diff": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P, _P]),

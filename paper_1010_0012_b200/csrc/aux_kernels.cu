@@ -1,35 +1,57 @@
 // Bookkeeping kernels around the message kernel: message init, value upload,
 // beliefs / MAP labels, directed-edge store gather, convergence delta.
 #include "aux_kernels.cuh"
+#include "band_kernel.cuh"   // Vec8Loader, lanes_sum / lanes_max
 
 namespace sbp {
 
 // bp.py:587-601: sum -> 1/M on real slots and 1 on ghost slots (no
 // neighbour: the product identity, so border nodes need no branches);
-// max -> 0.  Labels >= M are padding: 0 (sum) / -inf (max).
+// max -> 0.  Labels >= M are padding: 0 (sum) / -inf (max).  One warp per
+// node vector, 16-byte stores.  With ghosts_only the warp list is just the
+// border slots (2W + 2 rows vectors): the message kernels never write them
+// and overwrite every real slot, so this is all a buffer needs once.
 __global__ void init_msgs_kernel(float *msgs, int H, int W, int M, int Ms, int r0, int rows,
-                                 int domain) {
-    const long long per_slot = (long long)(rows + 2) * W * Ms;
-    const long long total = 4 * per_slot;
-    const float uni = 1.0f / (float)M;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(i % Ms);
-        const long long node = (i / Ms) % ((long long)(rows + 2) * W);
-        const int k = (int)(i / per_slot);
-        const int c = (int)(node % W);
-        const long long r = (long long)r0 + node / W - 1;
-        float v;
-        if (x >= M) {
-            v = domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
-        } else if (domain == SBP_MAX) {
-            v = 0.0f;
-        } else {
-            const bool ghost = (k == 0 && r <= 0) || (k == 1 && c == 0) ||
-                               (k == 2 && c == W - 1) || (k == 3 && r >= H - 1);
-            v = ghost ? 1.0f : uni;
+                                 int domain, int ghosts_only) {
+    const long long per_slot = (long long)(rows + 2) * W;   // node vectors per slot
+    const long long count = ghosts_only ? 2LL * W + 2LL * rows : 4 * per_slot;
+    const int lane = threadIdx.x & 31;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const float pad = domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    const bool top = r0 == 0, bottom = r0 + rows == H;
+    for (long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < count;
+         v += warps) {
+        int k;
+        long long lr, c;
+        if (!ghosts_only) {
+            k = (int)(v / per_slot);
+            lr = (v % per_slot) / W;
+            c = v % W;
+        } else if (v < W) {                       // slot 0, global row 0
+            if (!top) continue;
+            k = 0; lr = 1; c = v;
+        } else if (v < 2LL * W) {                 // slot 3, global row H-1
+            if (!bottom) continue;
+            k = 3; lr = rows; c = v - W;
+        } else if (v < 2LL * W + rows) {          // slot 1, column 0
+            k = 1; lr = 1 + (v - 2LL * W); c = 0;
+        } else {                                  // slot 2, column W-1
+            k = 2; lr = 1 + (v - 2LL * W - rows); c = W - 1;
         }
-        msgs[i] = v;
+        const long long r = (long long)r0 + lr - 1;
+        const bool ghost = (k == 0 && r <= 0) || (k == 1 && c == 0) ||
+                           (k == 2 && c == W - 1) || (k == 3 && r >= H - 1);
+        const float real = domain == SBP_MAX ? 0.0f : (ghost ? 1.0f : 1.0f / (float)M);
+        float4 *dst = reinterpret_cast<float4 *>(msgs + (k * per_slot + lr * W + c) * Ms);
+        for (int q = lane; q < Ms / 4; q += 32) {
+            const int x = 4 * q;
+            float4 val;
+            val.x = x + 0 < M ? real : pad;
+            val.y = x + 1 < M ? real : pad;
+            val.z = x + 2 < M ? real : pad;
+            val.w = x + 3 < M ? real : pad;
+            dst[q] = val;
+        }
     }
 }
 
@@ -60,111 +82,109 @@ __global__ void load_values_kernel(const double *src, float *dst, long long node
     }
 }
 
-// One warp per node, lanes stride the labels.  Sum: b = g * m0 * m1 * m2 * m3
-// in the order np.multiply.at applies them (bp.py:715-720; ghost slots are
-// exactly 1), rescaled by the running max after every factor so fp32 does
-// not underflow on peaked messages, Z = sum * prod(scales) in
-// f64, beliefs = b / sum.  Max: s = ln g + m0 + m1 + m2 + m3 - max
-// (bp.py:728-738).  Labels: argmax, lowest index on ties (bp.py:741-744).
-template <int DOM>
-__global__ void beliefs_kernel(const float *values, const float *msgs, int W, int M, int Ms,
-                               int rows, float *beliefs, double *normalizers, int *labels,
-                               unsigned long long *bad_node) {
+// Beliefs / max-marginals / labels.  LP lanes per node, 8 consecutive labels
+// per lane (LP * 8 = Ms), all five input vectors loaded up front with 256-bit
+// loads.  Sum: b = g * m0 * m1 * m2 * m3 in the order np.multiply.at applies
+// them (bp.py:715-720; ghost slots hold exactly 1), after every factor
+// rescaled by an exact power of two so the running max stays in [1, 2) (no
+// rounding, no underflow on peaked messages); Z = sum * 2^e in
+// f64; beliefs = b / sum.  Max: ln g + m0 + m1 + m2 + m3 - max in f64
+// (bp.py:728-738), rounded once.  Labels: argmax, lowest index on ties
+// (bp.py:741-744), taken on the values that are returned.
+template <int DOM, int LP>
+__global__ void __launch_bounds__(256) beliefs_kernel(const float *values, const float *msgs,
+                                                      int W, int M, int Ms, int rows,
+                                                      float *beliefs, double *normalizers,
+                                                      int *labels, unsigned long long *bad_node) {
+    constexpr int VL = 8;
     const long long slot = (long long)(rows + 2) * W * Ms;
     const int lane = threadIdx.x & 31;
+    const int j = lane % LP;
+    const int x0 = j * VL;
     const long long nodes = (long long)rows * W;
+    const long long groups = (nodes + (32 / LP) - 1) / (32 / LP);
     const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long n = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < nodes;
-         n += warps) {
-        const float *g = values + n * Ms;
-        const float *m = msgs + (n + W) * Ms;   // local row = global row + 1
-        double scale = 1.0;
-        float z = 0.0f, best = -__builtin_huge_valf();
-        int best_x = 0x7fffffff;
-        if (DOM == SBP_SUM) {
-            // pass 1: per-label product with rescaling; each lane keeps its labels
-            // in registers only for Ms <= 256 (8 per lane)
-            float b[8];
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < groups;
+         w += warps) {
+        long long n = w * (32 / LP) + lane / LP;
+        const bool valid = n < nodes;
+        if (!valid) n = nodes - 1;
+        float g[VL], m[4][VL];
+        Vec8Loader<VL>::load(g, values + n * Ms + x0);
+        const float *mp = msgs + (n + W) * Ms + x0;   // local row = global row + 1
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int x = lane + 32 * q;
-                b[q] = (x < M) ? g[x] : 0.0f;
-            }
+        for (int k = 0; k < 4; ++k) Vec8Loader<VL>::load(m[k], mp + k * slot);
+        float best = -__builtin_huge_valf();
+        int best_x = 0x7fffffff;
+        float out[VL];
+        if (DOM == SBP_SUM) {
+            float b[VL];
+            int e_tot = 0;
+#pragma unroll
+            for (int i = 0; i < VL; ++i) b[i] = g[i];
+#pragma unroll
             for (int k = 0; k < 4; ++k) {
                 float mx = 0.0f;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int x = lane + 32 * q;
-                    if (x < M) b[q] *= m[k * slot + x];
-                    mx = fmaxf(mx, b[q]);
+                for (int i = 0; i < VL; ++i) {
+                    b[i] *= m[k][i];
+                    mx = fmaxf(mx, b[i]);
                 }
-                for (int off = 16; off; off >>= 1)
-                    mx = fmaxf(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
-                // rescale by an exact power of two so the running max stays
-                // in [1, 2): no rounding, no drift towards the denormals
+                mx = lanes_max<LP>(mx);
                 if (mx > 0.0f) {
                     int e;
                     frexpf(mx, &e);
                     e -= 1;
                     if (e != 0) {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) b[q] = ldexpf(b[q], -e);
-                        scale = ldexp(scale, e);
+                        for (int i = 0; i < VL; ++i) b[i] = ldexpf(b[i], -e);
+                        e_tot += e;
                     }
                 }
             }
+            float z = 0.0f;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) z += b[q];
-            for (int off = 16; off; off >>= 1) z += __shfl_xor_sync(SBP_FULL_MASK, z, off);
+            for (int i = 0; i < VL; ++i) z += b[i];
+            z = lanes_sum<LP>(z);
             if (!(z > 0.0f)) {
-                if (lane == 0 && bad_node) atomicMin(bad_node, (unsigned long long)n);
+                if (valid && j == 0 && bad_node) atomicMin(bad_node, (unsigned long long)n);
                 continue;
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int x = lane + 32 * q;
-                if (x < M) {
-                    const float v = b[q] / z;
-                    if (beliefs) beliefs[n * M + x] = v;
-                    if (v > best) { best = v; best_x = x; }
-                }
-            }
-            if (lane == 0 && normalizers) normalizers[n] = (double)z * scale;
+            for (int i = 0; i < VL; ++i) out[i] = b[i] / z;
+            if (valid && j == 0 && normalizers) normalizers[n] = ldexp((double)z, e_tot);
         } else {
-            // scores in f64: ln g + m0 + m1 + m2 + m3 - max, rounded once
-            double s[8];
+            double sd[VL];
             double mx = -__builtin_huge_val();
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int x = lane + 32 * q;
-                if (x < M) {
-                    double v = (double)g[x];
-                    for (int k = 0; k < 4; ++k) v += (double)m[k * slot + x];
-                    s[q] = v;
-                    mx = fmax(mx, v);
-                } else {
-                    s[q] = -__builtin_huge_val();
-                }
+            for (int i = 0; i < VL; ++i) {
+                double v = (double)g[i];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) v += (double)m[k][i];
+                sd[i] = v;
+                if (x0 + i < M) mx = fmax(mx, v);
             }
-            for (int off = 16; off; off >>= 1)
+#pragma unroll
+            for (int off = 1; off < LP; off <<= 1)
                 mx = fmax(mx, __shfl_xor_sync(SBP_FULL_MASK, mx, off));
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int x = lane + 32 * q;
-                if (x < M) {
-                    const float v = (float)(s[q] - mx);
-                    if (beliefs) beliefs[n * M + x] = v;
-                    if (v > best) { best = v; best_x = x; }
-                }
+            for (int i = 0; i < VL; ++i) out[i] = (float)(sd[i] - mx);
+        }
+#pragma unroll
+        for (int i = 0; i < VL; ++i) {
+            const int x = x0 + i;
+            if (x < M) {
+                if (valid && beliefs) beliefs[n * M + x] = out[i];
+                if (out[i] > best) { best = out[i]; best_x = x; }
             }
         }
-        // argmax across lanes: larger value wins, lower label on ties
-        for (int off = 16; off; off >>= 1) {
+#pragma unroll
+        for (int off = 1; off < LP; off <<= 1) {
             const float ov = __shfl_xor_sync(SBP_FULL_MASK, best, off);
             const int ox = __shfl_xor_sync(SBP_FULL_MASK, best_x, off);
             if (ov > best || (ov == best && ox < best_x)) { best = ov; best_x = ox; }
         }
-        if (lane == 0 && labels) labels[n] = best_x == 0x7fffffff ? 0 : best_x;
+        if (valid && j == 0 && labels) labels[n] = best_x == 0x7fffffff ? 0 : best_x;
     }
 }
 
@@ -230,9 +250,10 @@ static unsigned grid_for(long long work, int block) {
 }
 
 cudaError_t launch_init_msgs(float *msgs, int H, int W, int M, int Ms, int r0, int rows,
-                             int domain, cudaStream_t s) {
-    init_msgs_kernel<<<grid_for(4LL * (rows + 2) * W * Ms, 256), 256, 0, s>>>(
-        msgs, H, W, M, Ms, r0, rows, domain);
+                             int domain, int ghosts_only, cudaStream_t s) {
+    const long long vecs = ghosts_only ? 2LL * W + 2LL * rows : 4LL * (rows + 2) * W;
+    init_msgs_kernel<<<grid_for(vecs * 32, 256), 256, 0, s>>>(msgs, H, W, M, Ms, r0, rows,
+                                                              domain, ghosts_only);
     return cudaGetLastError();
 }
 
@@ -242,17 +263,33 @@ cudaError_t launch_load_values(const double *src, float *dst, long long nodes, i
     return cudaGetLastError();
 }
 
+template <int DOM>
+static cudaError_t launch_beliefs_dom(const float *values, const float *msgs, int W, int M,
+                                      int Ms, int rows, float *beliefs, double *normalizers,
+                                      int *labels, unsigned long long *bad_node, cudaStream_t s) {
+    const long long lanes = (long long)rows * W * (Ms / 8);
+    const unsigned blocks = grid_for(lanes, 256);
+#define SBP_B(LPV)                                                                        \
+    case LPV:                                                                             \
+        beliefs_kernel<DOM, LPV><<<blocks, 256, 0, s>>>(values, msgs, W, M, Ms, rows,     \
+                                                        beliefs, normalizers, labels, bad_node); \
+        break;
+    switch (Ms / 8) {
+        SBP_B(1) SBP_B(2) SBP_B(4) SBP_B(8) SBP_B(16) SBP_B(32)
+    default: return cudaErrorInvalidValue;
+    }
+#undef SBP_B
+    return cudaGetLastError();
+}
+
 cudaError_t launch_beliefs(int domain, const float *values, const float *msgs, int W, int M,
                            int Ms, int rows, float *beliefs, double *normalizers, int *labels,
                            unsigned long long *bad_node, cudaStream_t s) {
-    const unsigned blocks = grid_for((long long)rows * W * 32, 256);
     if (domain == SBP_SUM)
-        beliefs_kernel<SBP_SUM><<<blocks, 256, 0, s>>>(values, msgs, W, M, Ms, rows, beliefs,
-                                                       normalizers, labels, bad_node);
-    else
-        beliefs_kernel<SBP_MAX><<<blocks, 256, 0, s>>>(values, msgs, W, M, Ms, rows, beliefs,
-                                                       normalizers, labels, bad_node);
-    return cudaGetLastError();
+        return launch_beliefs_dom<SBP_SUM>(values, msgs, W, M, Ms, rows, beliefs, normalizers,
+                                           labels, bad_node, s);
+    return launch_beliefs_dom<SBP_MAX>(values, msgs, W, M, Ms, rows, beliefs, normalizers,
+                                       labels, bad_node, s);
 }
 
 cudaError_t launch_gather_store(const float *msgs, int H, int W, int M, int Ms, float *out,

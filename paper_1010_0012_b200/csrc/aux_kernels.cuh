@@ -4,7 +4,7 @@
 namespace sbp {
 
 cudaError_t launch_init_msgs(float *msgs, int H, int W, int M, int Ms, int r0, int rows,
-                             int domain, cudaStream_t s);
+                             int domain, int ghosts_only, cudaStream_t s);
 cudaError_t launch_load_values(const double *src, float *dst, long long nodes, int M, int Ms,
                                int domain, cudaStream_t s);
 cudaError_t launch_beliefs(int domain, const float *values, const float *msgs, int W, int M,
@@ -22,6 +22,7 @@ struct EllArgs {
     unsigned long long *err;
     long long slot_stride;
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term, m_max;
+    int first;
     float fbar[2];
     const int *idx[2];
     const float *w[2];

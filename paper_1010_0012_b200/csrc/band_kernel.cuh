@@ -33,6 +33,7 @@ struct BandArgs {
     unsigned long long *err;
     long long slot_stride;  // (rows+2)*W*Ms
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term;
+    int first;   // iteration 0: incoming messages are the reference init, not read
     float fbar[2];
     float w[2][2 * SBP_MAX_R + 1];
 };
@@ -215,10 +216,24 @@ __global__ void __launch_bounds__(128) band_iter_kernel(const __grid_constant__ 
     float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
     Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
     const float *mi = a.msgs_in + node_l * a.Ms + x0;
-    Vec8Loader<VL>::load(m0, mi);
-    Vec8Loader<VL>::load(m1, mi + a.slot_stride);
-    Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
-    Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+    if (!a.first) {
+        Vec8Loader<VL>::load(m0, mi);
+        Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+        Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+        Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+    } else {
+        // bp.py:587-601 without touching memory: 1/M on real slots, the
+        // identity on ghost slots, padding 0 / -inf
+        const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+        float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+        }
+    }
 
     const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
     float h[VL];

@@ -77,11 +77,11 @@ int sbp_padded_labels(int M) {
     return ms;
 }
 
-int sbp_init_msgs(const sbp_grid *g, int domain, float *msgs, void *stream) {
+int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!msgs) return fail(SBP_EINVAL, "msgs is NULL");
     return cuda_status(sbp::launch_init_msgs(msgs, g->H, g->W, g->M, g->Ms, g->r0, g->rows,
-                                             domain, (cudaStream_t)stream),
+                                             domain, ghosts_only ? 1 : 0, (cudaStream_t)stream),
                        "sbp_init_msgs");
 }
 
@@ -95,7 +95,7 @@ int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst
 
 int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
                 const float *msgs_in, float *msgs_out, int lr_begin, int lr_end, int iteration,
-                unsigned long long *err, void *stream) {
+                int flags, unsigned long long *err, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!pot || !values || !msgs_in || !msgs_out || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (pot->domain != SBP_SUM && pot->domain != SBP_MAX) return fail(SBP_EINVAL, "bad domain");
@@ -123,6 +123,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.floor_term = pot->floor_term;
+        a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
         const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
         for (int o = 0; o < 2; ++o) {
             a.fbar[o] = pot->fbar[o];
@@ -145,6 +146,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.floor_term = pot->kind == SBP_POT_DENSE ? 0 : pot->floor_term;
         a.m_max = pot->m_max;
+        a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
         for (int o = 0; o < 2; ++o) {
             a.fbar[o] = pot->fbar[o];
             a.idx[o] = pot->ell_idx[o];

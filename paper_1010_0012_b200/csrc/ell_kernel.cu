@@ -107,7 +107,14 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
         const bool in = x < a.Ms;
         g[q] = in ? gp[x] : PAD;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m[k][q] = in ? mp[k * a.slot_stride + x] : PAD;
+        if (!a.first) {
+            for (int k = 0; k < 4; ++k) m[k][q] = in ? mp[k * a.slot_stride + x] : PAD;
+        } else {
+            const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+            for (int k = 0; k < 4; ++k)
+                m[k][q] = x >= a.M ? PAD
+                                   : (DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f);
+        }
     }
     float h[ELL_QMAX];
     const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;

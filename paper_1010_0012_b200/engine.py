@@ -197,8 +197,8 @@ class GridEngine:
             self.values = torch.empty((self.rows, self.W, self.Ms), dtype=torch.float32,
                                       device=self.device)
             self.upload_values(values)
-        self.cur = 0
-        self.iterations = 0
+        for buf in self.msgs:
+            self._init(buf, ghosts_only=True)
         self.reset()
 
     # -- setup -------------------------------------------------------------
@@ -237,17 +237,35 @@ class GridEngine:
                                          _ptr(self.values), _stream_handle()))
         self._staging = dev   # keep alive until the stream consumed it
 
-    def reset(self) -> None:
-        for buf in self.msgs:
-            L.check(self.lib.sbp_init_msgs(ctypes_ref(self.grid), self.dom, _ptr(buf),
-                                           _stream_handle()))
+    def _init(self, buf: torch.Tensor, ghosts_only: bool) -> None:
+        L.check(self.lib.sbp_init_msgs(ctypes_ref(self.grid), self.dom, 1 if ghosts_only else 0,
+                                       _ptr(buf), _stream_handle()))
+
+    def reset(self, full: bool = False) -> None:
+        """Start a new run from the reference initial messages (bp.py:587-601).
+
+        The ghost (border) slots of both buffers were set once at construction
+        and are never written by the iteration kernels; the first iteration
+        runs with SBP_ITER_FIRST and takes the uniform initial messages as
+        constants, so no per-run initialisation traffic is needed.  ``full``
+        materialises the initial messages in the current buffer (needed when
+        they are read: the convergence test after iteration 1, or a read-out
+        before any iteration).
+        """
         self.err.fill_(-1)
         self.cur = 0
         self.iterations = 0
+        self._init_valid = False
+        if full:
+            self._init(self.msgs[0], ghosts_only=False)
+            self._init_valid = True
 
     # -- iteration ---------------------------------------------------------
     @property
     def current(self) -> torch.Tensor:
+        if self.iterations == 0 and not self._init_valid:
+            self._init(self.msgs[self.cur], ghosts_only=False)
+            self._init_valid = True
         return self.msgs[self.cur]
 
     def iterate_rows(self, lr_begin: int, lr_end: int, stream: int | None = None) -> None:
@@ -258,7 +276,8 @@ class GridEngine:
         L.check(self.lib.sbp_iterate(
             ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
             _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), lr_begin, lr_end,
-            self.iterations, _ptr(self.err), _stream_handle() if stream is None else stream))
+            self.iterations, L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self.err),
+            _stream_handle() if stream is None else stream))
 
     def flip(self) -> None:
         self.cur = 1 - self.cur
@@ -436,8 +455,8 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
         store.stats = stats
         return store
     eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device)
-    if engine is not None:
-        eng.reset()
+    if engine is not None or convergence_tol is not None:
+        eng.reset(full=convergence_tol is not None)
     per_iter = 2 * int(model.n_edges)
     events: list = []
     for _ in range(n_sweeps):
