@@ -34,6 +34,7 @@ struct BandArgs {
     long long slot_stride;  // (rows+2)*W*Ms
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term;
     int first;   // iteration 0: incoming messages are the reference init, not read
+    int prefetch;  // L2-prefetch the next pixel group (persistent loop)
     float fbar[2];
     float w[2][2 * SBP_MAX_R + 1];
 };
@@ -196,15 +197,13 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&
     if (!ok && j == 0) report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
 
+// One warp-group of PPW = 32/LP nodes (flattened pixel group `grp`).
 template <int DOM, int VL, int LP, int R>
-__global__ void __launch_bounds__(128) band_iter_kernel(const __grid_constant__ BandArgs a) {
+__device__ __forceinline__ void band_group(const BandArgs &a, long long grp, long long npix) {
     constexpr int PPW = 32 / LP;
     const int lane = threadIdx.x & 31;
     const int j = lane % LP;
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
-    if (warp * PPW >= npix) return;  // warp-uniform
-    long long p = warp * PPW + lane / LP;
+    long long p = grp * PPW + lane / LP;
     const bool valid = p < npix;
     if (!valid) p = npix - 1;
     const int lr = a.lr_begin + (int)(p / a.W);
@@ -322,6 +321,42 @@ __global__ void __launch_bounds__(128) band_iter_kernel(const __grid_constant__ 
     }
 }
 
+// L2 prefetch of one pixel group's five input vectors (unary + 4 incoming
+// slots).  node_l and the value index are linear in the flattened pixel
+// index, so each vector of a group is one contiguous chunk.
+__device__ __forceinline__ void prefetch_group(const BandArgs &a, long long grp, long long npix,
+                                               int ppw) {
+    const int lane = threadIdx.x & 31;
+    if (lane > 4 || (lane < 4 && a.first)) return;
+    const long long p0 = grp * ppw;
+    if (p0 >= npix) return;
+    const long long n = (npix - p0 < ppw ? npix - p0 : ppw);
+    const unsigned bytes = (unsigned)(n * a.Ms * 4);
+    const float *src = lane == 4
+        ? a.values + ((long long)(a.lr_begin - 1) * a.W + p0) * a.Ms
+        : a.msgs_in + lane * a.slot_stride + ((long long)a.lr_begin * a.W + p0) * a.Ms;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Persistent grid-stride kernel: each warp walks pixel groups grp, grp + T,
+// ... (T = resident warps) and prefetches its next group into L2 before
+// computing the current one, keeping HBM requests in flight during the
+// band arithmetic.
+template <int DOM, int VL, int LP, int R>
+__global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : 3))
+band_iter_kernel(const __grid_constant__ BandArgs a) {
+    constexpr int PPW = 32 / LP;
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long ngroups = (npix + PPW - 1) / PPW;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (a.prefetch && grp < ngroups) prefetch_group(a, grp, npix, PPW);
+    for (; grp < ngroups; grp += nwarps) {
+        if (a.prefetch && grp + nwarps < ngroups) prefetch_group(a, grp + nwarps, npix, PPW);
+        band_group<DOM, VL, LP, R>(a, grp, npix);
+    }
+}
+
 }  // namespace sbp
 
 namespace sbp {
@@ -331,10 +366,22 @@ using BandLaunchFn = cudaError_t (*)(const BandArgs &, cudaStream_t);
 template <int DOM, int VL, int LP, int R>
 cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
     constexpr int PPW = 32 / LP;
+    static int resident = 0;   // blocks of this instantiation per SM
+    static int sms = 0;
+    if (!resident) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, band_iter_kernel<DOM, VL, LP, R>,
+                                                      128, 0);
+        if (resident < 1) resident = 1;
+    }
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long warps = (npix + PPW - 1) / PPW;
-    const long long blocks = (warps + 3) / 4;
+    long long blocks = (warps + 3) / 4;
     if (blocks <= 0) return cudaSuccess;
+    const long long cap = (long long)sms * resident;
+    if (blocks > cap) blocks = cap;
     band_iter_kernel<DOM, VL, LP, R><<<(unsigned)blocks, 128, 0, s>>>(a);
     return cudaGetLastError();
 }

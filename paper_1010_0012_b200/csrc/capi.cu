@@ -41,12 +41,21 @@ int check_grid(const sbp_grid *g) {
 
 const int kRadii[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32};
 
+int band_prefetch() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBP_PREFETCH");
+        v = e ? atoi(e) != 0 : 0;   // measured slower on C4 (tools/sweep_r01.sh)
+    }
+    return v;
+}
+
 int band_vl(int Ms) {
     if (const char *e = getenv("SBP_BAND_VL")) {
         int v = atoi(e);
         if ((v == 8 || v == 16) && v <= Ms) return v;
     }
-    return Ms >= 128 ? 16 : 8;
+    return Ms >= 256 ? 16 : 8;   // sweep on B200: VL=8 best up to Ms=128
 }
 
 sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R) {
@@ -124,6 +133,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.floor_term = pot->floor_term;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
+        a.prefetch = band_prefetch();
         const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
         for (int o = 0; o < 2; ++o) {
             a.fbar[o] = pot->fbar[o];
