@@ -79,8 +79,10 @@ typedef struct {
     float band_w[2][2 * SBP_MAX_R + 1];   /* BAND: w[o][d + R] (residual | log value) */
     const int32_t *ell_idx[2];            /* ELL: device [m_max][Ms], x_i per (k, x_j) */
     const float *ell_w[2];                /* ELL: device [m_max][Ms] */
-    const float *dense_t[2];              /* reserved (DENSE currently runs on the ELL
-                                             arrays with m_max = M, idx[k][x] = k) */
+    const float *dense_t[2];              /* DENSE: device [Ms][Ms] per orientation,
+                                             f(x_i = k, x_j = x) at [k][x] (tiled kernel,
+                                             Ms >= 32); smaller Ms runs the ELL arrays with
+                                             m_max = M, idx[k][x] = k */
 } sbp_potential;
 
 SBP_API int sbp_version(void);

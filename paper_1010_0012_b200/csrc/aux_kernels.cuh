@@ -29,6 +29,17 @@ struct EllArgs {
 };
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s);
 
+struct DenseArgs {
+    const float *values;
+    const float *msgs_in;
+    float *msgs_out;
+    unsigned long long *err;
+    long long slot_stride;
+    int H, W, M, Ms, r0, lr_begin, lr_end, iteration, first;
+    const float *t[2];   // [Ms][Ms] per orientation: f(x_i = k, x_j = x) at [k][x]
+};
+cudaError_t launch_dense(int domain, const DenseArgs &a, cudaStream_t s);
+
 
 
 }  // namespace sbp

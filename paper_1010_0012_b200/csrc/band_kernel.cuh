@@ -124,11 +124,13 @@ __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const fl
 }
 
 // One outgoing direction: fast update + normalisation + store.
-template <int DOM, int VL, int LP, int R, int DIR>
-__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int j,
-                                               int x0, bool active, long long node_l,
+// O (orientation) is compile-time so every weight is a constant-bank operand;
+// DIR is a compile-time constant in the unrolled kernel and a runtime value in
+// the rolled one (store slot / step / edge id only).
+template <int DOM, int VL, int LP, int R, int O>
+__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int DIR,
+                                               int j, int x0, bool active, long long node_l,
                                                long long r, int c) {
-    constexpr int O = dir_orient(DIR);
     float out[VL];
     if (DOM == SBP_SUM) {
         float s = 0.0f;
@@ -245,24 +247,24 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
         if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ((g[i] * m1[i]) * m2[i]) * m3[i];
-            emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = (ab[i] * m2[i]) * m3[i];
-            emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
 #pragma unroll
         for (int i = 0; i < VL; ++i) ab[i] = ab[i] * m1[i];                 // g m0 m1
         if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ab[i] * m3[i];
-            emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ab[i] * m2[i];
-            emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     } else {
         // Max-sum: h = ln g + sum of three messages.  Its entries can reach
@@ -283,7 +285,7 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
                 two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, 3>(a, h, j, x0, valid && has_u, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
 #pragma unroll
@@ -293,7 +295,7 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
                 two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, 1>(a, h, j, x0, valid && has_l, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
 #pragma unroll
         for (int i = 0; i < VL; ++i) {                                       // g + m0 + m1
@@ -307,7 +309,7 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
                 two_sum(sa[i], m3[i], s2[i], e); e2[i] = ea[i] + e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, 0>(a, h, j, x0, valid && has_r, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
 #pragma unroll
@@ -316,8 +318,102 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
                 two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, 2>(a, h, j, x0, valid && has_d, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
+    }
+}
+
+// Rolled variant for potentials whose two orientations carry the same band
+// (symmetric f, e.g. every truncated-linear / quadratic config): one copy of
+// the fully unrolled band serves all four directions (runtime loop), cutting
+// the instruction footprint 4x -- the unrolled kernel spills the I-cache for
+// wide bands (ncu: 34 % of issue slots lost to instruction fetch at R = 32).
+template <int DOM, int VL, int LP, int R>
+__device__ __forceinline__ void band_group_rolled(const BandArgs &a, long long grp,
+                                                  long long npix) {
+    constexpr int PPW = 32 / LP;
+    const int lane = threadIdx.x & 31;
+    const int j = lane % LP;
+    long long p = grp * PPW + lane / LP;
+    const bool valid = p < npix;
+    if (!valid) p = npix - 1;
+    const int lr = a.lr_begin + (int)(p / a.W);
+    const int c = (int)(p % a.W);
+    const long long r = (long long)a.r0 + lr - 1;
+    const long long node_l = (long long)lr * a.W + c;
+    const int x0 = j * VL;
+
+    float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
+    Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
+    const float *mi = a.msgs_in + node_l * a.Ms + x0;
+    if (!a.first) {
+        Vec8Loader<VL>::load(m0, mi);
+        Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+        Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+        Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+    } else {
+        const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+        float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+        }
+    }
+    // bit d: the node has a neighbour in direction d (no local arrays:
+    // runtime-indexed arrays would live in local memory)
+    const unsigned has = (c + 1 < a.W ? 1u : 0u) | (c > 0 ? 2u : 0u) |
+                         (r + 1 < a.H ? 4u : 0u) | (r > 0 ? 8u : 0u);
+    // prefixes shared by the directions (same association as the unrolled
+    // kernel, so both variants give identical bits)
+    float pa[VL], pb[VL], ea[VL], eb[VL];
+#pragma unroll
+    for (int i = 0; i < VL; ++i) {
+        if (DOM == SBP_SUM) {
+            pa[i] = g[i] * m0[i];
+            pb[i] = pa[i] * m1[i];
+        } else {
+            float t, e;
+            two_sum(g[i], m0[i], pa[i], ea[i]);
+            two_sum(pa[i], m1[i], t, e);
+            pb[i] = t;
+            eb[i] = ea[i] + e;
+        }
+    }
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+        const int dir = (0x2013 >> (4 * k)) & 0xF;   // order 3, 1, 0, 2
+        const bool hd = (has >> dir) & 1u;
+        if (!__any_sync(SBP_FULL_MASK, valid && hd)) continue;
+        float h[VL];
+        if (DOM == SBP_SUM) {
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                h[i] = dir == 3 ? ((g[i] * m1[i]) * m2[i]) * m3[i]
+                     : dir == 1 ? (pa[i] * m2[i]) * m3[i]
+                     : dir == 0 ? pb[i] * m3[i] : pb[i] * m2[i];
+        } else {
+            float s2[VL], e2[VL];
+#pragma unroll
+            for (int i = 0; i < VL; ++i) {
+                float t, e;
+                if (dir == 3) {
+                    two_sum(g[i], m1[i], s2[i], e2[i]);
+                    two_sum(s2[i], m2[i], t, e); s2[i] = t; e2[i] += e;
+                    two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
+                } else if (dir == 1) {
+                    two_sum(pa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
+                    two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
+                } else {
+                    two_sum(pb[i], dir == 0 ? m3[i] : m2[i], s2[i], e);
+                    e2[i] = eb[i] + e;
+                }
+            }
+            shift_compensated<VL, LP>(s2, e2, h);
+        }
+        emit_direction<DOM, VL, LP, R, 0>(a, h, dir, j, x0, valid && hd, node_l, r, c);
     }
 }
 
@@ -342,7 +438,7 @@ __device__ __forceinline__ void prefetch_group(const BandArgs &a, long long grp,
 // ... (T = resident warps) and prefetches its next group into L2 before
 // computing the current one, keeping HBM requests in flight during the
 // band arithmetic.
-template <int DOM, int VL, int LP, int R>
+template <int DOM, int VL, int LP, int R, bool ROLLED>
 __global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : 3))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
@@ -353,7 +449,8 @@ band_iter_kernel(const __grid_constant__ BandArgs a) {
     if (a.prefetch && grp < ngroups) prefetch_group(a, grp, npix, PPW);
     for (; grp < ngroups; grp += nwarps) {
         if (a.prefetch && grp + nwarps < ngroups) prefetch_group(a, grp + nwarps, npix, PPW);
-        band_group<DOM, VL, LP, R>(a, grp, npix);
+        if constexpr (ROLLED) band_group_rolled<DOM, VL, LP, R>(a, grp, npix);
+        else band_group<DOM, VL, LP, R>(a, grp, npix);
     }
 }
 
@@ -363,7 +460,7 @@ namespace sbp {
 
 using BandLaunchFn = cudaError_t (*)(const BandArgs &, cudaStream_t);
 
-template <int DOM, int VL, int LP, int R>
+template <int DOM, int VL, int LP, int R, bool ROLLED>
 cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
     constexpr int PPW = 32 / LP;
     static int resident = 0;   // blocks of this instantiation per SM
@@ -372,8 +469,8 @@ cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, band_iter_kernel<DOM, VL, LP, R>,
-                                                      128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &resident, band_iter_kernel<DOM, VL, LP, R, ROLLED>, 128, 0);
         if (resident < 1) resident = 1;
     }
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
@@ -382,7 +479,7 @@ cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
-    band_iter_kernel<DOM, VL, LP, R><<<(unsigned)blocks, 128, 0, s>>>(a);
+    band_iter_kernel<DOM, VL, LP, R, ROLLED><<<(unsigned)blocks, 128, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -390,7 +487,7 @@ cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
 // smallest listed R >= r (extra taps carry weight 0 / -inf: exact no-ops).
 #define SBP_BAND_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
 
-template <int MS, int DOM, int VL>
+template <int MS, int DOM, int VL, bool ROLLED>
 BandLaunchFn pick_band_r(int R) {
     if constexpr (VL > MS) {
         return nullptr;
@@ -398,7 +495,7 @@ BandLaunchFn pick_band_r(int R) {
         switch (R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
-        if constexpr (RR < MS) return &launch_band<DOM, VL, MS / VL, RR>; \
+        if constexpr (RR < MS) return &launch_band<DOM, VL, MS / VL, RR, ROLLED>; \
         else return nullptr;
             SBP_BAND_RADII(SBP_CASE)
 #undef SBP_CASE
@@ -407,14 +504,14 @@ BandLaunchFn pick_band_r(int R) {
     }
 }
 
-template <int MS>
-BandLaunchFn pick_band(int dom, int vl, int R) {
-    if (dom == SBP_SUM) {
-        if (vl == 8) return pick_band_r<MS, SBP_SUM, 8>(R);
-        if (vl == 16) return pick_band_r<MS, SBP_SUM, 16>(R);
-    } else {
-        if (vl == 8) return pick_band_r<MS, SBP_MAX, 8>(R);
-        if (vl == 16) return pick_band_r<MS, SBP_MAX, 16>(R);
+// VL = 16 is compiled only where the sweeps chose it (sum, Ms >= 128); the
+// max domain always runs VL = 8 (its TwoSum state spills at VL = 16).
+template <int MS, int DOM>
+BandLaunchFn pick_band_dom(int vl, int R, int rolled) {
+    if (vl == 8) return rolled ? pick_band_r<MS, DOM, 8, true>(R) : pick_band_r<MS, DOM, 8, false>(R);
+    if constexpr (DOM == SBP_SUM && MS >= 128) {
+        if (vl == 16)
+            return rolled ? pick_band_r<MS, DOM, 16, true>(R) : pick_band_r<MS, DOM, 16, false>(R);
     }
     return nullptr;
 }

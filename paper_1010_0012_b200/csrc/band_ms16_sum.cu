@@ -1,0 +1,5 @@
+// Band-kernel instantiations: padded label stride Ms = 16, sum domain.
+#include "band_kernel.cuh"
+namespace sbp {
+template BandLaunchFn pick_band_dom<16, SBP_SUM>(int, int, int);
+}

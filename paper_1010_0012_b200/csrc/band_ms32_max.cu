@@ -1,0 +1,5 @@
+// Band-kernel instantiations: padded label stride Ms = 32, max domain.
+#include "band_kernel.cuh"
+namespace sbp {
+template BandLaunchFn pick_band_dom<32, SBP_MAX>(int, int, int);
+}

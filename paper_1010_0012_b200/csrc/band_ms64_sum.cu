@@ -1,0 +1,5 @@
+// Band-kernel instantiations: padded label stride Ms = 64, sum domain.
+#include "band_kernel.cuh"
+namespace sbp {
+template BandLaunchFn pick_band_dom<64, SBP_SUM>(int, int, int);
+}

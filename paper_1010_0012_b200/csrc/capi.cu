@@ -8,8 +8,13 @@
 #include "band_kernel.cuh"
 
 namespace sbp {
+template <int MS, int DOM>
+BandLaunchFn pick_band_dom(int vl, int R, int rolled);
 template <int MS>
-BandLaunchFn pick_band(int dom, int vl, int R);
+BandLaunchFn pick_band(int dom, int vl, int R, int rolled) {
+    return dom == SBP_SUM ? pick_band_dom<MS, SBP_SUM>(vl, R, rolled)
+                          : pick_band_dom<MS, SBP_MAX>(vl, R, rolled);
+}
 }
 
 namespace {
@@ -50,22 +55,33 @@ int band_prefetch() {
     return v;
 }
 
-int band_vl(int Ms) {
+int band_vl(int Ms, int domain) {
     if (const char *e = getenv("SBP_BAND_VL")) {
         int v = atoi(e);
-        if ((v == 8 || v == 16) && v <= Ms) return v;
+        if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128)) return v;
     }
-    return Ms >= 256 ? 16 : 8;   // sweep on B200: VL=8 best up to Ms=128
+    // B200 sweep (tools/sweep_r01.sh): VL = 8 up to Ms = 128 and for max-sum
+    return (domain == SBP_SUM && Ms >= 256) ? 16 : 8;
 }
 
-sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R) {
+// Rolled (single band copy) kernel for symmetric potentials with R >= this.
+int band_roll_min_r() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBP_ROLL_MIN_R");
+        v = e ? atoi(e) : 12;
+    }
+    return v;
+}
+
+sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled) {
     switch (Ms) {
-    case 8: return sbp::pick_band<8>(dom, vl, R);
-    case 16: return sbp::pick_band<16>(dom, vl, R);
-    case 32: return sbp::pick_band<32>(dom, vl, R);
-    case 64: return sbp::pick_band<64>(dom, vl, R);
-    case 128: return sbp::pick_band<128>(dom, vl, R);
-    case 256: return sbp::pick_band<256>(dom, vl, R);
+    case 8: return sbp::pick_band<8>(dom, vl, R, rolled);
+    case 16: return sbp::pick_band<16>(dom, vl, R, rolled);
+    case 32: return sbp::pick_band<32>(dom, vl, R, rolled);
+    case 64: return sbp::pick_band<64>(dom, vl, R, rolled);
+    case 128: return sbp::pick_band<128>(dom, vl, R, rolled);
+    case 256: return sbp::pick_band<256>(dom, vl, R, rolled);
     default: return nullptr;
     }
 }
@@ -119,8 +135,13 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         int Rk = 0;
         for (int r : kRadii)
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
-        const int vl = band_vl(g->Ms);
-        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk) : nullptr;
+        const int vl = band_vl(g->Ms, pot->domain);
+        bool sym = pot->fbar[0] == pot->fbar[1];
+        for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
+            sym = pot->band_w[0][k] == pot->band_w[1][k] ||
+                  (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
+        const int rolled = sym && Rk >= band_roll_min_r();
+        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk, rolled) : nullptr;
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
         sbp::BandArgs a;
@@ -141,6 +162,20 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
             for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
         }
         return cuda_status(fn(a, s), "sbp_iterate(band)");
+    }
+    if (pot->kind == SBP_POT_DENSE && pot->dense_t[0] && pot->dense_t[1] && g->Ms >= 32) {
+        sbp::DenseArgs a;
+        a.values = values;
+        a.msgs_in = msgs_in;
+        a.msgs_out = msgs_out;
+        a.err = err;
+        a.slot_stride = slot;
+        a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
+        a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
+        a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
+        a.t[0] = pot->dense_t[0];
+        a.t[1] = pot->dense_t[1];
+        return cuda_status(sbp::launch_dense(pot->domain, a, s), "sbp_iterate(dense)");
     }
     if (pot->kind == SBP_POT_ELL || pot->kind == SBP_POT_DENSE) {
         if (pot->m_max < 0 || !pot->ell_idx[0] || !pot->ell_idx[1] || !pot->ell_w[0] ||

@@ -218,6 +218,12 @@ class GridEngine:
             for o in range(2):
                 s.ell_idx[o] = idx[o].data_ptr()
                 s.ell_w[o] = w[o].data_ptr()
+            if plan.dense_t is not None:
+                t = torch.from_numpy(np.ascontiguousarray(plan.dense_t, dtype=np.float32)).to(
+                    self.device)
+                plan.device_arrays.append(t)
+                for o in range(2):
+                    s.dense_t[o] = t[o].data_ptr()
         return s
 
     def upload_values(self, values: np.ndarray | torch.Tensor | None = None) -> None:

@@ -43,6 +43,7 @@ class PotentialPlan:
     m_max: int = 0
     ell_idx: np.ndarray | None = None       # (2, m_max, Ms) int32
     ell_w: np.ndarray | None = None         # (2, m_max, Ms) f64
+    dense_t: np.ndarray | None = None       # (2, Ms, Ms) f64, f(x_i=k, x_j=x) at [o, k, x]
     madds_per_update: int = 0
     device_arrays: list = field(default_factory=list)
 
@@ -121,11 +122,13 @@ def plan_potential(pot, domain: str, kernel: str, M: int, Ms: int,
         tabs = (table, table.T)     # orientation o: f_o(x_i = k, x_j = x) at [k][x]
         idx = np.zeros((2, M, Ms), dtype=np.int32)
         w = np.full((2, M, Ms), pad, dtype=np.float64)
+        dense = np.full((2, Ms, Ms), pad, dtype=np.float64)
         for o in range(2):
             idx[o] = np.arange(M, dtype=np.int32)[:, None]
             w[o, :, :M] = tabs[o]
+            dense[o, :M, :M] = tabs[o]
         return PotentialPlan(L.SBP_POT_DENSE, dom, kernel, 0, M, Ms, (0.0, 0.0), m_max=M,
-                             ell_idx=idx, ell_w=w, madds_per_update=M * M)
+                             ell_idx=idx, ell_w=w, dense_t=dense, madds_per_update=M * M)
     if not _is_sparse(use):
         raise TypeError(f"kernel={kernel!r} requires SparseTruncatedPotential, "
                         f"got {type(pot).__name__}")

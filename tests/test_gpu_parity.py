@@ -241,3 +241,38 @@ def test_c4_full_size_invariants():
     assert (cur[~real] == 1).all()
     lab = eng.labels()
     assert lab.shape == (H * W,) and int(lab.min()) >= 0 and int(lab.max()) < model.M
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5_T9"])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_dense_tiled_kernel(name, domain):
+    """The tiled dense comparison kernel (Ms >= 32) against the oracle's
+    reference standard update."""
+    model = synth.build_config_model(synth.CONFIGS[name], height=20, width=36)
+    check_run(model, 6, domain, "standard")
+
+
+def test_fast_equals_standard_max_bitwise_m256():
+    model = synth.build_config_model(synth.CONFIGS["C5_T9"], height=12, width=20)
+    a = sbp.run_sweeps(model, 8, kernel="fast", domain="max", schedule=SYNC).data
+    b = sbp.run_sweeps(model, 8, kernel="standard", domain="max", schedule=SYNC).data
+    np.testing.assert_array_equal(a, b)
+
+
+def _run_subprocess(env_extra, name, domain, iters, out):
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, str(root / "tools" / "dump_case.py"), name, domain,
+                    str(iters), "24", "40", str(out)], check=True, env=env, cwd=str(root))
+    return np.load(out)
+
+
+@pytest.mark.parametrize("name,domain", [("C4", "sum"), ("C3", "max"), ("C5_T33", "sum")])
+def test_rolled_and_unrolled_kernels_agree_bitwise(tmp_path, name, domain):
+    a = _run_subprocess({"SBP_ROLL_MIN_R": "1"}, name, domain, 7, tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_ROLL_MIN_R": "99"}, name, domain, 7, tmp_path / "b.npy")
+    np.testing.assert_array_equal(a, b)
