@@ -101,13 +101,21 @@ __device__ __forceinline__ float band_h(const float (&h)[VL], int t, int j) {
     return j + q < LP ? v : PAD;
 }
 
+// Three-input max (sm_100 FMNMX3): exact, same NaN rule as fmaxf.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 // Knuth TwoSum: a + b = s + e exactly (no FMA contraction: adds only).
-// Infinite sums (-inf log unaries / padding) carry e = 0.
+// With -inf operands (log of a zero unary / potential entry, label padding)
+// e becomes NaN; once a partial sum is -inf it stays -inf (there is no +inf),
+// so the NaN is discarded once, on the final sum, in shift_compensated.
 __device__ __forceinline__ void two_sum(float a, float b, float &s, float &e) {
     s = a + b;
     const float bp = s - a;
-    const float ee = (a - (s - bp)) + (b - bp);
-    e = isfinite(s) ? ee : 0.0f;
+    e = (a - (s - bp)) + (b - bp);
 }
 
 // h'[i] = (s[i] - c) + e[i] with c = max over the node's labels of s.
@@ -120,7 +128,7 @@ __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const fl
     c = lanes_max<LP>(c);
     if (!isfinite(c)) c = 0.0f;
 #pragma unroll
-    for (int i = 0; i < VL; ++i) h[i] = (s[i] - c) + e[i];
+    for (int i = 0; i < VL; ++i) h[i] = (s[i] - c) + (isfinite(s[i]) ? e[i] : 0.0f);
 }
 
 // One outgoing direction: fast update + normalisation + store.
@@ -150,15 +158,35 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&
         for (int i = 0; i < VL; ++i) out[i] = base;
     }
     // Band, streamed in ascending x_i: term (x_i = x0+t) reaches out[i] at d = t - i.
+    if (DOM == SBP_SUM) {
 #pragma unroll
-    for (int t = -R; t < VL + R; ++t) {
-        const float hv = band_h<DOM, VL, LP, R>(h, t, j);
+        for (int t = -R; t < VL + R; ++t) {
+            const float hv = band_h<DOM, VL, LP, R>(h, t, j);
 #pragma unroll
-        for (int i = 0; i < VL; ++i) {
-            const int d = t - i;
-            if (d < -R || d > R) continue;
-            if (DOM == SBP_SUM) out[i] = fmaf(a.w[O][d + R], hv, out[i]);
-            else out[i] = fmaxf(out[i], a.w[O][d + R] + hv);
+            for (int i = 0; i < VL; ++i) {
+                const int d = t - i;
+                if (d < -R || d > R) continue;
+                out[i] = fmaf(a.w[O][d + R], hv, out[i]);
+            }
+        }
+    } else {
+        // two taps per FMNMX3 (the max is exact: any grouping gives the same bits)
+#pragma unroll
+        for (int t = -R; t < VL + R; t += 2) {
+            const float hv0 = band_h<DOM, VL, LP, R>(h, t, j);
+            const float hv1 = t + 1 < VL + R ? band_h<DOM, VL, LP, R>(h, t + 1, j) : 0.0f;
+#pragma unroll
+            for (int i = 0; i < VL; ++i) {
+                const int d0 = t - i, d1 = t + 1 - i;
+                const bool in0 = d0 >= -R && d0 <= R;
+                const bool in1 = t + 1 < VL + R && d1 >= -R && d1 <= R;
+                if (in0 && in1)
+                    out[i] = fmax3(out[i], a.w[O][d0 + R] + hv0, a.w[O][d1 + R] + hv1);
+                else if (in0)
+                    out[i] = fmaxf(out[i], a.w[O][d0 + R] + hv0);
+                else if (in1)
+                    out[i] = fmaxf(out[i], a.w[O][d1 + R] + hv1);
+            }
         }
     }
     // Normalise (numba_kernels.py:248-271); padded labels stay 0 / -inf.
@@ -495,7 +523,8 @@ BandLaunchFn pick_band_r(int R) {
         switch (R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
-        if constexpr (RR < MS) return &launch_band<DOM, VL, MS / VL, RR, ROLLED>; \
+        if constexpr (RR < MS && (!ROLLED || RR >= 24))                   \
+            return &launch_band<DOM, VL, MS / VL, RR, ROLLED>;             \
         else return nullptr;
             SBP_BAND_RADII(SBP_CASE)
 #undef SBP_CASE

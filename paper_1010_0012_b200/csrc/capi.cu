@@ -69,7 +69,7 @@ int band_roll_min_r() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("SBP_ROLL_MIN_R");
-        v = e ? atoi(e) : 12;
+        v = e ? atoi(e) : 24;   // sweep (tools/sweep_r01b.sh): wins at R = 32, loses at R <= 16
     }
     return v;
 }
@@ -140,7 +140,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
             sym = pot->band_w[0][k] == pot->band_w[1][k] ||
                   (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
-        const int rolled = sym && Rk >= band_roll_min_r();
+        const int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;   // compiled for R >= 24
         sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk, rolled) : nullptr;
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
