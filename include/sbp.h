@@ -16,6 +16,8 @@
  *                         one SYNCHRONOUS iteration of all directed updates
  *                         of a row range: _grid_h_* (:194-227) -> _fast_* /
  *                         _std_* / _pruned_* (:35-101) -> _norm_*_store (:248-271)
+ *   sbp_sweep          <- bp.py:492-503 + numba_kernels.py:274-407: one canonical
+ *                         sequential sweep (the reference default schedule)
  *   sbp_beliefs        <- bp.py:711-744      `compute_beliefs`,
  *                                            `compute_max_marginals`, `map_labels`
  *   sbp_gather_store   <- bp.py:604-617      `_grid_store_to_messages`
@@ -108,6 +110,14 @@ SBP_API int sbp_load_values(const sbp_grid *g, int domain, const double *src, fl
 SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
                         const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
                         int iteration, int flags, unsigned long long *err, void *stream);
+
+/* One canonical SEQUENTIAL sweep in place (the reference's default schedule,
+ * bp.py:492-503 -> numba_kernels.py:274-407): passes L->R, R->L, T->B, B->T,
+ * each a set of independent row / column chains updated in order.  Full grid,
+ * band potentials.  Failures: err = min(sweep << 40 | pass << 38 |
+ * line * line_len + position), i.e. the reference's first failing message. */
+SBP_API int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                      float *msgs, int sweep, unsigned long long *err, void *stream);
 
 /* Per-node beliefs (sum: normalised product, max: max-normalised scores),
  * normalisers Z (sum only, f64) and argmax labels (lowest index on ties).

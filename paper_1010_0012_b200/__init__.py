@@ -7,7 +7,7 @@ Model construction mirrors ``sparsebp.mrf``; ``run_sweeps`` /
 """
 from .model import (DensePotential, GridMrf, SparseTruncatedPotential, build_grid_mrf,
                     grid_edges, sparse_from_dense, truncated_linear_potential)
-from .engine import (SYNCHRONOUS, BeliefTable, DegenerateBeliefError, DegenerateMessageError,
+from .engine import (SEQUENTIAL, SYNCHRONOUS, BeliefTable, DegenerateBeliefError, DegenerateMessageError,
                      GridEngine, MessageStore, SweepStats, UnsafePotentialError,
                      compute_beliefs, compute_max_marginals, map_labels, run_sweeps)
 

@@ -59,6 +59,8 @@ _PROTOS = {
     "sbp_load_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P]),
     "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
                          _i, _i, _i, _i, _P, _P]),
+    "sbp_sweep": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _i, _P,
+                       _P]),
     "sbp_beliefs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P, _P, _P, _P, _P]),
     "sbp_gather_store": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P]),
     "sbp_max_abs_diff": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P, _P]),

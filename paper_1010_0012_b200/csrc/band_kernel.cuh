@@ -35,6 +35,7 @@ struct BandArgs {
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term;
     int first;   // iteration 0: incoming messages are the reference init, not read
     int prefetch;  // L2-prefetch the next pixel group (persistent loop)
+    int pass;      // sequential mode: pass direction 0..3 (chain_kernel.cuh)
     float fbar[2];
     float w[2][2 * SBP_MAX_R + 1];
 };
@@ -135,11 +136,12 @@ __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const fl
 // O (orientation) is compile-time so every weight is a constant-bank operand;
 // DIR is a compile-time constant in the unrolled kernel and a runtime value in
 // the rolled one (store slot / step / edge id only).
+// The message of one directed edge from its exclusion vector h: the fast
+// update (floor term + band) and the reference normalisation.  Returns
+// whether the message could be normalised.
 template <int DOM, int VL, int LP, int R, int O>
-__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int DIR,
-                                               int j, int x0, bool active, long long node_l,
-                                               long long r, int c) {
-    float out[VL];
+__device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)[VL], int j,
+                                             int x0, float (&out)[VL]) {
     if (DOM == SBP_SUM) {
         float s = 0.0f;
 #pragma unroll
@@ -219,6 +221,15 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&
 #pragma unroll
         for (int i = 0; i < VL; ++i) out[i] -= mx;
     }
+    return ok;
+}
+
+template <int DOM, int VL, int LP, int R, int O>
+__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int DIR,
+                                               int j, int x0, bool active, long long node_l,
+                                               long long r, int c) {
+    float out[VL];
+    const bool ok = band_message<DOM, VL, LP, R, O>(a, h, j, x0, out);
     if (!active) return;
     const long long W = a.W;
     const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;

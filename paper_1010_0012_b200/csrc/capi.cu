@@ -17,6 +17,11 @@ BandLaunchFn pick_band(int dom, int vl, int R, int rolled) {
 }
 }
 
+namespace sbp {
+template <int MS, int DOM>
+BandLaunchFn pick_chain(int R);
+}
+
 namespace {
 
 thread_local char g_err[512] = "";
@@ -200,6 +205,48 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         return cuda_status(sbp::launch_ell(pot->domain, a, s), "sbp_iterate(ell)");
     }
     return fail(SBP_EINVAL, "unknown potential kind %d", pot->kind);
+}
+
+int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, float *msgs,
+              int sweep, unsigned long long *err, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!pot || !values || !msgs || !err) return fail(SBP_EINVAL, "NULL pointer");
+    if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "sequential sweeps need the full grid");
+    if (pot->kind != SBP_POT_BAND)
+        return fail(SBP_EUNSUPPORTED, "sequential sweeps support band potentials only");
+    if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
+    if (sweep < 0 || sweep >= (1 << 23)) return fail(SBP_EINVAL, "bad sweep index");
+    int Rk = 0;
+    for (int r : kRadii)
+        if (r >= pot->R && r < g->Ms) { Rk = r; break; }
+    sbp::BandLaunchFn fn = nullptr;
+    if (Rk) {
+#define SBP_C(MSV)                                                                          \
+    case MSV:                                                                               \
+        fn = pot->domain == SBP_SUM ? sbp::pick_chain<MSV, SBP_SUM>(Rk)                     \
+                                    : sbp::pick_chain<MSV, SBP_MAX>(Rk);                    \
+        break;
+        switch (g->Ms) { SBP_C(8) SBP_C(16) SBP_C(32) SBP_C(64) SBP_C(128) SBP_C(256) default: break; }
+#undef SBP_C
+    }
+    if (!fn) return fail(SBP_EUNSUPPORTED, "no chain kernel for Ms=%d R=%d", g->Ms, pot->R);
+    sbp::BandArgs a;
+    memset(&a, 0, sizeof a);
+    a.values = values;
+    a.msgs_in = msgs;
+    a.msgs_out = msgs;
+    a.err = err;
+    a.slot_stride = (long long)(g->rows + 2) * g->W * g->Ms;
+    a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = 0;
+    a.lr_begin = 1; a.lr_end = g->H + 1; a.iteration = sweep;
+    a.floor_term = pot->floor_term;
+    const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    for (int o = 0; o < 2; ++o) {
+        a.fbar[o] = pot->fbar[o];
+        for (int k = 0; k < 2 * SBP_MAX_R + 1; ++k) a.w[o][k] = pad;
+        for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
+    }
+    return cuda_status(fn(a, (cudaStream_t)stream), "sbp_sweep");
 }
 
 int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float *msgs,

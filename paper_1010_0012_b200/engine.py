@@ -12,12 +12,14 @@ with the reference's exception types and attributes
 (``DegenerateMessageError.edge``, ``DegenerateBeliefError.node``,
 ``UnsafePotentialError``) and validation (bp.py:411-433).
 
-Schedule: the GPU runs the SYNCHRONOUS (Jacobi) schedule -- all directed
-messages of iteration t+1 from those of iteration t.  The reference's
-default is its canonical in-place sequential sweep (bp.py:630-633), which
-gives different numbers, so ``schedule`` must be passed
-explicitly as ``"synchronous"``; the default raises instead of silently
-changing semantics.
+Schedules: ``schedule=None`` (or the reference's canonical
+``SweepSchedule``) runs the reference's own in-place sequential sweep
+(bp.py:630-633: L->R, R->L, T->B, B->T passes, each a set of independent
+row/column chains) -- a true drop-in of the default.  ``schedule=
+"synchronous"`` runs the Jacobi schedule of the benchmark -- all directed
+messages of iteration t+1 from those of iteration t, fully parallel and
+HBM-bound.  The two give different numbers; both are pinned to
+the oracle.
 
 Every device computation goes through libsbp.so (hand-written sm_100a
 kernels, ``csrc/``); torch provides device memory, streams and events only.
@@ -34,11 +36,12 @@ import torch
 from . import _lib as L
 from .plan import PotentialPlan, plan_potential
 
-__all__ = ["SYNCHRONOUS", "DegenerateMessageError", "DegenerateBeliefError",
+__all__ = ["SYNCHRONOUS", "SEQUENTIAL", "DegenerateMessageError", "DegenerateBeliefError",
            "UnsafePotentialError", "SweepStats", "BeliefTable", "MessageStore", "GridEngine",
            "run_sweeps", "compute_beliefs", "compute_max_marginals", "map_labels"]
 
 SYNCHRONOUS = "synchronous"
+SEQUENTIAL = "sequential"
 KERNELS = ("standard", "fast", "pruned")
 DOMAINS = ("sum", "max")
 
@@ -164,7 +167,8 @@ class GridEngine:
     """
 
     def __init__(self, model, domain: str = "sum", kernel: str = "fast", device=None,
-                 r0: int = 0, rows: int | None = None, values: np.ndarray | None = None):
+                 r0: int = 0, rows: int | None = None, values: np.ndarray | None = None,
+                 schedule: str = SYNCHRONOUS):
         if not torch.cuda.is_available():
             raise RuntimeError("the GPU grid engine needs a CUDA device (no CPU fallback)")
         self.lib = L.lib()
@@ -178,6 +182,9 @@ class GridEngine:
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         pot = _shared_potential(model)
         _validate(model, kernel, domain, pot)
+        self.schedule = schedule
+        if schedule == SEQUENTIAL and (r0 != 0 or (rows is not None and rows != self.H)):
+            raise NotImplementedError("sequential sweeps run on the whole grid (no strips)")
         self.r0 = r0
         self.rows = self.H - r0 if rows is None else rows
         self.Ms = self.lib.sbp_padded_labels(self.M)
@@ -188,6 +195,10 @@ class GridEngine:
         self.plan: PotentialPlan | None = None
         if pot is not None:
             self.plan = plan_potential(pot, domain, kernel, self.M, self.Ms)
+            if schedule == SEQUENTIAL and self.plan.kind != L.SBP_POT_BAND:
+                raise NotImplementedError(
+                    "the GPU sequential schedule supports banded (Toeplitz) potentials with the "
+                    f"fast/pruned kernels; got a {self.plan.kind_name} plan (kernel={kernel!r})")
             self._pot_struct = self._make_pot_struct(self.plan)
         with torch.cuda.device(self.device):
             shape = (4, self.rows + 2, self.W, self.Ms)
@@ -262,7 +273,7 @@ class GridEngine:
         self.cur = 0
         self.iterations = 0
         self._init_valid = False
-        if full:
+        if full or self.schedule == SEQUENTIAL:   # in-place sweeps read every slot
             self._init(self.msgs[0], ghosts_only=False)
             self._init_valid = True
 
@@ -289,7 +300,31 @@ class GridEngine:
         self.cur = 1 - self.cur
         self.iterations += 1
 
+    def sweep(self) -> None:
+        """One canonical sequential sweep in place (reference ``_run_grid``)."""
+        if self.plan is not None:
+            L.check(self.lib.sbp_sweep(ctypes_ref(self.grid), ctypes_ref(self._pot_struct),
+                                       _ptr(self.values), _ptr(self.msgs[0]), self.iterations,
+                                       _ptr(self.err), _stream_handle()))
+        self.iterations += 1
+
+    def snapshot(self) -> None:
+        """Keep a copy of the current messages (sequential convergence test)."""
+        self.msgs[1].copy_(self.msgs[0])
+
     def step(self, n: int = 1, events: list | None = None) -> None:
+        if self.schedule == SEQUENTIAL:
+            for _ in range(n):
+                ev0 = ev1 = None
+                if events is not None:
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev0.record()
+                self.sweep()
+                if events is not None:
+                    ev1 = torch.cuda.Event(enable_timing=True)
+                    ev1.record()
+                    events.append((ev0, ev1))
+            return
         for _ in range(n):
             if events is not None:
                 ev0 = torch.cuda.Event(enable_timing=True)
@@ -316,11 +351,24 @@ class GridEngine:
 
     def raise_if_degenerate(self) -> None:
         e = self.error()
-        if e is not None:
-            it, d = e
-            i, j = _edge_endpoints(self.H, self.W, d)
+        if e is None:
+            return
+        it, d = e
+        if self.schedule == SEQUENTIAL:
+            # key: sweep << 40 | pass << 38 | line * line_len + position
+            direction, idx = (d >> 38) & 3, d & ((1 << 38) - 1)
+            H, W = self.H, self.W
+            lines_len = W - 1 if direction <= 1 else H - 1
+            line, pos = divmod(idx, lines_len)
+            stride, step, origin = {0: (W, 1, 0), 1: (W, -1, W - 1), 2: (1, W, 0),
+                                    3: (1, -W, (H - 1) * W)}[direction]
+            src = line * stride + origin + pos * step
             raise DegenerateMessageError(
-                f"degenerate message on edge {i}->{j} (synchronous iteration {it})", edge=(i, j))
+                f"degenerate message on edge {src}->{src + step} (pass direction {direction})",
+                edge=(int(src), int(src + step)))
+        i, j = _edge_endpoints(self.H, self.W, d)
+        raise DegenerateMessageError(
+            f"degenerate message on edge {i}->{j} (synchronous iteration {it})", edge=(i, j))
 
     # -- read-out ----------------------------------------------------------
     def beliefs_device(self, want_beliefs: bool = True, want_labels: bool = True):
@@ -436,21 +484,30 @@ class MessageStore:
             assert (self.data.max(axis=1) == 0.0).all(), "max-domain message max is not exactly 0"
 
 
+def _schedule_mode(schedule) -> str:
+    """None / the reference canonical SweepSchedule -> sequential (bp.py:647-648);
+    "synchronous" -> Jacobi."""
+    if schedule is None or schedule in (SEQUENTIAL, "canonical"):
+        return SEQUENTIAL
+    if schedule == SYNCHRONOUS:
+        return SYNCHRONOUS
+    if getattr(schedule, "grid_canonical", False):
+        return SEQUENTIAL
+    raise NotImplementedError(
+        "custom SweepSchedule pass orders are not supported on the GPU; use None (the "
+        "canonical sequential sweep) or 'synchronous'")
+
+
 def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
                schedule=None, convergence_tol: float | None = None, device=None,
                engine: GridEngine | None = None) -> MessageStore:
-    """Run ``n_sweeps`` synchronous iterations on the GPU (reference bp.py:620-703).
+    """Run ``n_sweeps`` sweeps on the GPU (reference bp.py:620-703).
 
-    One synchronous iteration updates every directed edge once, like one
-    reference sweep, but from the previous iteration's messages only.
+    ``schedule=None`` -- the reference's canonical in-place sequential sweep;
+    ``schedule="synchronous"`` -- one Jacobi iteration per sweep (every
+    directed edge once, from the previous iteration's messages only).
     """
-    if schedule is None:
-        raise NotImplementedError(
-            "the GPU engine runs the synchronous (Jacobi) schedule; the reference default is "
-            "its sequential in-place sweep, which gives different messages. Pass "
-            "schedule='synchronous' to opt in.")
-    if schedule != SYNCHRONOUS:
-        raise NotImplementedError(f"unsupported schedule {schedule!r}; use 'synchronous'")
+    mode = _schedule_mode(schedule)
     if n_sweeps < 0:
         raise ValueError(f"n_sweeps must be >= 0, got {n_sweeps}")
     pot = _shared_potential(model) if model.n_edges else None
@@ -460,12 +517,15 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
         store = MessageStore(model, domain, engine=None)
         store.stats = stats
         return store
-    eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device)
+    eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device,
+                                                       schedule=mode)
     if engine is not None or convergence_tol is not None:
         eng.reset(full=convergence_tol is not None)
     per_iter = 2 * int(model.n_edges)
     events: list = []
     for _ in range(n_sweeps):
+        if mode == SEQUENTIAL and convergence_tol is not None:
+            eng.snapshot()
         eng.step(1, events=events)
         stats.sweeps_run += 1
         stats.n_updates += per_iter

@@ -135,7 +135,10 @@ def test_grid_edges_reference_order():
 def test_run_sweeps_validation_without_gpu():
     model = synth.build_config_model(synth.CONFIGS["C1"], height=4, width=6)
     with pytest.raises(NotImplementedError):
-        sbp.run_sweeps(model, 2)                       # default (sequential) schedule
+        sbp.run_sweeps(model, 2, schedule=object())     # custom pass orders
+    if not __import__("torch").cuda.is_available():
+        with pytest.raises(RuntimeError):               # no CPU fallback
+            sbp.run_sweeps(model, 2)
     with pytest.raises(ValueError):
         sbp.run_sweeps(model, 2, kernel="bogus", schedule="synchronous")
     with pytest.raises(ValueError):
