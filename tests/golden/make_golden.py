@@ -376,6 +376,12 @@ def main():
     deg = sparsebp.build_grid_mrf(1, 2, 2, np.array([[1.0, 0.0], [1.0, 1.0]]), pot)
     add_sync_case("sync_degenerate_sum", deg, "sum", "fast", 3)
     add_seq_case("seq_degenerate_sum", deg, "sum", "fast", 3)
+    # the same failure with a banded (Toeplitz) potential: only d = +1 is stored
+    bpot = sparsebp.SparseTruncatedPotential(2, 0.0, np.array([0, 1, 1]), np.array([1]),
+                                             np.array([1.0]))
+    bdeg = sparsebp.build_grid_mrf(2, 3, 2, np.array([[1.0, 0.0]] * 6), bpot)
+    add_sync_case("sync_degenerate_band_sum", bdeg, "sum", "fast", 3)
+    add_seq_case("seq_degenerate_band_sum", bdeg, "sum", "fast", 3)
 
     # --- chains vs exact enumeration (BP is exact on trees) ------------------
     for (W, M, seed) in [(6, 3, 1), (5, 4, 2)]:

@@ -149,9 +149,10 @@ def test_deterministic_and_store_layout():
     s1.check_normalized(atol=1e-5)
 
 
-def test_degenerate_message_raises_with_edge():
-    e = MAN["cases"]["sync_degenerate_sum"]
-    model, _ = load_case("sync_degenerate_sum")
+@pytest.mark.parametrize("name", ["sync_degenerate_sum", "sync_degenerate_band_sum"])
+def test_degenerate_message_raises_with_edge(name):
+    e = MAN["cases"][name]
+    model, _ = load_case(name)
     with pytest.raises(sbp.DegenerateMessageError) as ei:
         sbp.run_sweeps(model, e["iters"], schedule=SYNC)
     ids = e["degenerate"]["directed_edge_ids"]

@@ -66,8 +66,8 @@ def test_reduced_configs_sequential(name, domain, sweeps):
 
 
 def test_sequential_degenerate_edge_matches_reference():
-    e = MAN["cases"]["seq_degenerate_sum"]
-    model, _ = load_case("seq_degenerate_sum")
+    e = MAN["cases"]["seq_degenerate_band_sum"]
+    model, _ = load_case("seq_degenerate_band_sum")
     with pytest.raises(sbp.DegenerateMessageError) as ei:
         sbp.run_sweeps(model, e["sweeps"])
     assert list(ei.value.edge) == e["degenerate_edge"]
