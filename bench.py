@@ -312,7 +312,7 @@ def run_ours(args, cfg):
         "config": config_dict(cfg, args, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_for("band_iter_kernel"),
-                     "peak_source": peak_src, "kernel": "band_iter_kernel<sum,16,8,7>",
+                     "peak_source": peak_src, "kernel": eng.kernel_name,
                      "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": B / world,
                      "flops_per_launch": F / world,
                      "fp32_frac_nominal": (F / world) / (kern_ms / 1e3) / 1e12 / FP32_NOMINAL_TFLOPS},

@@ -119,6 +119,11 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
 SBP_API int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values,
                       float *msgs, int sweep, unsigned long long *err, void *stream);
 
+/* Name of the kernel instantiation sbp_iterate (sequential = 0) or sbp_sweep
+ * (sequential = 1) would launch for this grid and potential. */
+SBP_API int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential,
+                          char *buf, int len);
+
 /* Per-node beliefs (sum: normalised product, max: max-normalised scores),
  * normalisers Z (sum only, f64) and argmax labels (lowest index on ties).
  * Any of beliefs / normalizers / labels may be NULL.  bad_node receives

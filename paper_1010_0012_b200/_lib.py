@@ -61,6 +61,8 @@ _PROTOS = {
                          _i, _i, _i, _i, _P, _P]),
     "sbp_sweep": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _i, _P,
                        _P]),
+    "sbp_plan_name": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _i,
+                           ctypes.c_char_p, _i]),
     "sbp_beliefs": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P, _P, _P, _P, _P]),
     "sbp_gather_store": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P]),
     "sbp_max_abs_diff": (_i, [ctypes.POINTER(SbpGrid), _P, _P, _P, _P]),

@@ -65,8 +65,10 @@ int band_vl(int Ms, int domain) {
         int v = atoi(e);
         if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128)) return v;
     }
-    // B200 sweep (tools/sweep_r01.sh): VL = 8 up to Ms = 128 and for max-sum
-    return (domain == SBP_SUM && Ms >= 256) ? 16 : 8;
+    // B200 A/B (tools/ab_vl.sh): at Ms = 128 VL = 8 is 1.6 % faster per cold
+    // launch but VL = 16 (fewer shuffles per label, less power) holds ~5 %
+    // better under the sustained power cap; max-sum always VL = 8
+    return (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
 }
 
 // Rolled (single band copy) kernel for symmetric potentials with R >= this.
@@ -247,6 +249,35 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
         for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
     }
     return cuda_status(fn(a, (cudaStream_t)stream), "sbp_sweep");
+}
+
+int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, char *buf,
+                  int len) {
+    if (int rc = check_grid(g)) return rc;
+    if (!pot || !buf || len < 1) return fail(SBP_EINVAL, "NULL pointer");
+    const char *dom = pot->domain == SBP_SUM ? "sum" : "max";
+    if (pot->kind == SBP_POT_BAND) {
+        int Rk = 0;
+        for (int r : kRadii)
+            if (r >= pot->R && r < g->Ms) { Rk = r; break; }
+        if (sequential) {
+            snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
+        } else {
+            const int vl = band_vl(g->Ms, pot->domain);
+            bool sym = pot->fbar[0] == pot->fbar[1];
+            for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
+                sym = pot->band_w[0][k] == pot->band_w[1][k] ||
+                      (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
+            const int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;
+            snprintf(buf, len, "band_iter_kernel<%s,VL=%d,LP=%d,R=%d,%s>", dom, vl, g->Ms / vl, Rk,
+                     rolled ? "rolled" : "unrolled");
+        }
+    } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
+        snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
+    } else {
+        snprintf(buf, len, "ell_iter_kernel<%s>", dom);
+    }
+    return SBP_OK;
 }
 
 int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float *msgs,

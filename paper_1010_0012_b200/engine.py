@@ -254,6 +254,17 @@ class GridEngine:
                                          _ptr(self.values), _stream_handle()))
         self._staging = dev   # keep alive until the stream consumed it
 
+    @property
+    def kernel_name(self) -> str:
+        """The kernel instantiation this engine launches per iteration / sweep."""
+        if self.plan is None:
+            return "none"
+        import ctypes
+        buf = ctypes.create_string_buffer(128)
+        L.check(self.lib.sbp_plan_name(ctypes_ref(self.grid), ctypes_ref(self._pot_struct),
+                                       1 if self.schedule == SEQUENTIAL else 0, buf, 128))
+        return buf.value.decode()
+
     def _init(self, buf: torch.Tensor, ghosts_only: bool) -> None:
         L.check(self.lib.sbp_init_msgs(ctypes_ref(self.grid), self.dom, 1 if ghosts_only else 0,
                                        _ptr(buf), _stream_handle()))
