@@ -327,10 +327,42 @@ def run_ours(args, cfg):
 
 
 def e2e_public_api(args, cfg, torch):
-    """run_sweeps + map_labels on a host model (pinned f64 unaries): H2D of the
-    values and D2H of the labels are inside the timed region."""
+    """End to end through the public API with host buffers, two ways:
+
+    * stereo pipeline (the reference's ``sparsebp stereo`` path, cli.py:121-136):
+      pinned uint8 image pair -> ``build_stereo_mrf`` -> ``run_sweeps`` ->
+      ``map_labels``; unaries are built on the device from the images;
+    * model unaries: a model holding pinned f64 unaries -> ``run_sweeps`` ->
+      ``map_labels`` (3.2 GB of f64 unaries cross PCIe each run).
+    H2D inputs and the D2H labels are inside both timed regions.
+    """
     import paper_1010_0012_b200 as sbp
     from paper_1010_0012_b200 import synth
+    reps = max(1, min(args.steps, 3))
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            out = fn()
+        return (time.perf_counter() - t0) / reps, out
+
+    left, right, _ = synth.noisy_stereo_pair(cfg.height, cfg.width, cfg.M, cfg.sigma, 0)
+    imgs = []
+    for img in (left, right):
+        t = torch.empty(img.shape, dtype=torch.uint8, pin_memory=True)
+        t.numpy()[...] = img
+        imgs.append(t.numpy())
+    params = sbp.StereoParams(M=cfg.M, alpha=cfg.alpha, T_b=cfg.T, beta=cfg.beta, T_u=cfg.T_u)
+
+    def stereo_once():
+        model = sbp.build_stereo_mrf(imgs[0], imgs[1], params)
+        store = sbp.run_sweeps(model, args.iters, domain=args.domain, schedule="synchronous")
+        return sbp.map_labels(store)
+
+    dt_s, labels = timed(stereo_once)
+
     values = synth.config_values(cfg, args.domain)
     pinned = torch.empty(values.shape, dtype=torch.float64, pin_memory=True)
     pinned.numpy()[...] = values
@@ -342,21 +374,23 @@ def e2e_public_api(args, cfg, torch):
         model = sbp.GridMrf(cfg.height, cfg.width, cfg.M, np.exp(host), cfg.build_potential(),
                             log_unaries=host)
 
-    def once():
+    def unary_once():
         store = sbp.run_sweeps(model, args.iters, domain=args.domain, schedule="synchronous")
         return sbp.map_labels(store)
 
-    for _ in range(1):
-        once()
-    torch.cuda.synchronize()
-    reps = max(1, min(args.steps, 3))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        labels = once()
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": cfg.n_directed * args.iters / dt, "unit": "updates/s",
-            "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(labels.size * 4),
-            "ms_per_step": dt * 1e3, "api": "run_sweeps(schedule='synchronous') + map_labels"}
+    dt_u, labels_u = timed(unary_once)
+    assert (labels_u == labels).mean() > 0.999   # same problem, two input routes
+    E = cfg.n_directed * args.iters
+    return {"value": E / dt_s, "unit": "updates/s",
+            "h2d_bytes_per_step": int(imgs[0].nbytes + imgs[1].nbytes),
+            "d2h_bytes_per_step": int(labels.size * 4), "ms_per_step": dt_s * 1e3,
+            "api": "build_stereo_mrf(left, right) + run_sweeps(schedule='synchronous') + "
+                   "map_labels; unaries built on the device",
+            "model_unaries": {"value": E / dt_u, "unit": "updates/s",
+                              "h2d_bytes_per_step": int(host.nbytes),
+                              "d2h_bytes_per_step": int(labels_u.size * 4),
+                              "ms_per_step": dt_u * 1e3,
+                              "api": "run_sweeps(GridMrf with pinned f64 unaries) + map_labels"}}
 
 
 def main():

@@ -11,6 +11,7 @@
  *   sbp_init_msgs      <- bp.py:587-601      `_grid_store_init`
  *   sbp_load_values    <- bp.py:488          values_in = unaries | log_unaries
  *                                            (f64 host model -> padded f32 device)
+ *   sbp_stereo_values  <- stereo.py:82-99,120-125 unary field on the device
  *   sbp_iterate        <- bp.py:492-503 + numba_kernels.py:296-316,364-384
  *                         (`_run_grid` -> `grid_pass_{sum,max}_{fast,standard,pruned}`);
  *                         one SYNCHRONOUS iteration of all directed updates
@@ -101,6 +102,13 @@ SBP_API int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float 
 
 /* f64 [rows][W][M] (device) -> padded f32 values [rows][W][Ms]. */
 SBP_API int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream);
+
+/* Stereo unaries straight from the image pair (stereo.py:82-99,120-125):
+ * left/right are device [rows][W] uint8 of this strip's rows; dst as in
+ * sbp_load_values (sum: exp(-energy); max: -energy shifted by the node max). */
+SBP_API int sbp_stereo_values(const sbp_grid *g, int domain, const uint8_t *left,
+                              const uint8_t *right, double beta, double T_u, float *dst,
+                              void *stream);
 
 /* One synchronous iteration over local rows [lr_begin, lr_end) (1-based
  * strip rows; a full grid is r0 = 0, rows = H, lr in [1, H+1)).  With

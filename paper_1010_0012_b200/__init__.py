@@ -11,6 +11,9 @@ from .engine import (SEQUENTIAL, SYNCHRONOUS, BeliefTable, DegenerateBeliefError
                      GridEngine, MessageStore, SweepStats, UnsafePotentialError,
                      compute_beliefs, compute_max_marginals, map_labels, run_sweeps)
 
+from .stereo import (GrayImage, StereoParams, build_stereo_mrf, disparity_to_image,
+                     random_dot_pair, stereo_unary_field)
+
 MrfModel = GridMrf
 
 __version__ = "0.1.0"

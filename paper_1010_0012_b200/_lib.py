@@ -57,6 +57,8 @@ _PROTOS = {
     "sbp_padded_labels": (_i, [_i]),
     "sbp_init_msgs": (_i, [ctypes.POINTER(SbpGrid), _i, _i, _P, _P]),
     "sbp_load_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P]),
+    "sbp_stereo_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, ctypes.c_double,
+                               ctypes.c_double, _P, _P]),
     "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
                          _i, _i, _i, _i, _P, _P]),
     "sbp_sweep": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _i, _P,

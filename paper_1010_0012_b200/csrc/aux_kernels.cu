@@ -310,3 +310,61 @@ cudaError_t launch_max_abs_diff(const float *a, const float *b, int W, int M, in
 }
 
 }  // namespace sbp
+
+namespace sbp {
+
+// Stereo unary field on the device (reference stereo.py:82-99, 120-125; the
+// SURVEY 8f #3 "GPU unary builder"): node (r, c) of the right image, label x:
+//     energy = beta * min(|R(r, c) - L(r, c + x)|, T_u)   (c + x < W)
+//              beta * T_u                                  (out of frame)
+// sum: exp(-energy); max: -energy shifted by the node's max -- computed in
+// f64 like the reference, rounded once to f32.  One warp per node.
+__global__ void stereo_values_kernel(const unsigned char *left, const unsigned char *right,
+                                     long long rows, int W, int M, int Ms, double beta,
+                                     double T_u, int domain, float *dst) {
+    const int lane = threadIdx.x & 31;
+    const long long nodes = rows * W;
+    const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long n = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < nodes;
+         n += warps) {
+        const long long r = n / W;
+        const int c = (int)(n % W);
+        const int rv = right[r * W + c];
+        const unsigned char *lrow = left + r * W;
+        const double full = beta * T_u;
+        double emin = __builtin_huge_val();
+        if (domain == SBP_MAX) {
+            for (int x = lane; x < M; x += 32) {
+                const double e = c + x < W ? beta * fmin((double)abs(rv - (int)lrow[c + x]), T_u)
+                                           : full;
+                emin = fmin(emin, e);
+            }
+            for (int off = 16; off; off >>= 1)
+                emin = fmin(emin, __shfl_xor_sync(SBP_FULL_MASK, emin, off));
+        }
+        float *d = dst + n * Ms;
+        for (int x = lane; x < Ms; x += 32) {
+            float v;
+            if (x >= M) {
+                v = domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+            } else {
+                const double e = c + x < W ? beta * fmin((double)abs(rv - (int)lrow[c + x]), T_u)
+                                           : full;
+                v = domain == SBP_SUM ? (float)exp(-e) : (float)(-e - (-emin));
+            }
+            d[x] = v;
+        }
+    }
+}
+
+cudaError_t launch_stereo_values(const unsigned char *left, const unsigned char *right,
+                                 long long rows, int W, int M, int Ms, double beta, double T_u,
+                                 int domain, float *dst, cudaStream_t s) {
+    long long b = (rows * W * 32 + 255) / 256;
+    if (b > 148LL * 32) b = 148LL * 32;
+    stereo_values_kernel<<<(unsigned)(b < 1 ? 1 : b), 256, 0, s>>>(left, right, rows, W, M, Ms,
+                                                                   beta, T_u, domain, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace sbp

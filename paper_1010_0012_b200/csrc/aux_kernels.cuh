@@ -12,6 +12,9 @@ cudaError_t launch_beliefs(int domain, const float *values, const float *msgs, i
                            unsigned long long *bad_node, cudaStream_t s);
 cudaError_t launch_gather_store(const float *msgs, int H, int W, int M, int Ms, float *out,
                                 cudaStream_t s);
+cudaError_t launch_stereo_values(const unsigned char *left, const unsigned char *right,
+                                 long long rows, int W, int M, int Ms, double beta, double T_u,
+                                 int domain, float *dst, cudaStream_t s);
 cudaError_t launch_max_abs_diff(const float *a, const float *b, int W, int M, int Ms, int rows,
                                 float *out, cudaStream_t s);
 

@@ -125,6 +125,17 @@ int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst
                        "sbp_load_values");
 }
 
+int sbp_stereo_values(const sbp_grid *g, int domain, const uint8_t *left, const uint8_t *right,
+                      double beta, double T_u, float *dst, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!left || !right || !dst) return fail(SBP_EINVAL, "NULL pointer");
+    if (!(beta > 0) || !(T_u > 0)) return fail(SBP_EINVAL, "beta and T_u must be > 0");
+    return cuda_status(sbp::launch_stereo_values(left, right, (long long)g->rows, g->W, g->M,
+                                                 g->Ms, beta, T_u, domain, dst,
+                                                 (cudaStream_t)stream),
+                       "sbp_stereo_values");
+}
+
 int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
                 const float *msgs_in, float *msgs_out, int lr_begin, int lr_end, int iteration,
                 int flags, unsigned long long *err, void *stream) {

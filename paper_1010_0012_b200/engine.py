@@ -237,8 +237,25 @@ class GridEngine:
                     s.dense_t[o] = t[o].data_ptr()
         return s
 
+    def upload_stereo(self) -> None:
+        """Image pair -> unary table on the device (sbp_stereo_values): the
+        H2D traffic is the two uint8 images of this strip's rows."""
+        left, right, beta, T_u = self.model.stereo_source
+        sl = slice(self.r0, self.r0 + self.rows)
+        dev = []
+        for img in (left, right):
+            t = torch.from_numpy(np.ascontiguousarray(img[sl]))
+            dev.append(t.to(self.device, non_blocking=t.is_pinned()))
+        L.check(self.lib.sbp_stereo_values(ctypes_ref(self.grid), self.dom, _ptr(dev[0]),
+                                           _ptr(dev[1]), beta, T_u, _ptr(self.values),
+                                           _stream_handle()))
+        self._staging = dev
+
     def upload_values(self, values: np.ndarray | torch.Tensor | None = None) -> None:
         """Host f64 unaries (sum) / log unaries (max) -> padded f32 device table."""
+        if values is None and getattr(self.model, "stereo_source", None) is not None:
+            self.upload_stereo()
+            return
         if values is None:
             src = self.model.unaries if self.domain == "sum" else self.model.log_unaries
             values = src[self.r0 * self.W:(self.r0 + self.rows) * self.W]

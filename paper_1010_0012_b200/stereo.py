@@ -1,0 +1,151 @@
+"""Stereo front end: image pair -> grid MRF whose unaries are built on the GPU.
+
+Mirrors the reference's stereo API (``sparsebp.stereo``, stereo.py:28-140):
+``GrayImage``, ``StereoParams``, ``build_stereo_mrf``, ``stereo_unary_field``,
+``disparity_to_image``.  The model returned by ``build_stereo_mrf`` carries the
+image pair; the engine uploads the two uint8 images (2 bytes per pixel) and
+computes the (H*W, M) unary table on the device (``sbp_stereo_values``,
+SURVEY 8f #3) instead of shipping 8*M bytes per pixel of host f64 unaries.
+The host ``unaries`` / ``log_unaries`` arrays are still available, computed
+lazily on first access with the reference formula, for callers that read them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .model import GridMrf, truncated_linear_potential
+from .synth import random_dot_pair as _random_dot_pair
+from .synth import stereo_unary_field as _unary_field
+
+__all__ = ["GrayImage", "StereoParams", "StereoMrf", "build_stereo_mrf", "stereo_unary_field",
+           "disparity_to_image", "random_dot_pair"]
+
+
+@dataclass(frozen=True, eq=False)
+class GrayImage:
+    """Row-major 8-bit grayscale image (reference stereo.py:28-52)."""
+
+    pixels: np.ndarray
+
+    def __post_init__(self) -> None:
+        px = np.asarray(self.pixels)
+        if px.ndim != 2 or px.shape[0] < 1 or px.shape[1] < 1:
+            raise ValueError(f"pixels must be a non-empty 2-D array, got shape {px.shape}")
+        if px.dtype != np.uint8:
+            if not np.issubdtype(px.dtype, np.integer) or px.min() < 0 or px.max() > 255:
+                raise ValueError("intensities must be integers in [0, 255]")
+            px = px.astype(np.uint8)
+        px = np.ascontiguousarray(px)
+        px.setflags(write=False)
+        object.__setattr__(self, "pixels", px)
+
+    @property
+    def height(self) -> int:
+        return self.pixels.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.pixels.shape[1]
+
+
+@dataclass(frozen=True)
+class StereoParams:
+    """Reference defaults (stereo.py:55-79): M=16, alpha=1, T_b=2, beta=0.05,
+    T_u=20, 10 sweeps.  BASELINE's configs use beta=0.1, T_u=255."""
+
+    M: int = 16
+    alpha: float = 1.0
+    T_b: float = 2.0
+    beta: float = 0.05
+    T_u: float = 20.0
+    n_sweeps: int = 10
+
+    def __post_init__(self) -> None:
+        if self.M < 1:
+            raise ValueError(f"M must be >= 1, got {self.M}")
+        for name in ("alpha", "T_b", "beta", "T_u"):
+            if not getattr(self, name) > 0:
+                raise ValueError(f"{name} must be > 0, got {getattr(self, name)}")
+        if self.n_sweeps < 1:
+            raise ValueError(f"n_sweeps must be >= 1, got {self.n_sweeps}")
+
+
+def _pixels(img) -> np.ndarray:
+    return img.pixels if hasattr(img, "pixels") else np.asarray(img, dtype=np.uint8)
+
+
+def stereo_unary_field(left, right, params: StereoParams):
+    """Host (N, M) unaries and analytic logs (reference stereo.py:120-125)."""
+    return _unary_field(_pixels(left), _pixels(right), params.M, params.beta, params.T_u)
+
+
+class StereoMrf(GridMrf):
+    """Grid MRF over right-image pixels whose unaries derive from an image pair.
+
+    ``stereo_source`` = (left, right, beta, T_u) lets the engine build the
+    unary table on the device; ``unaries`` / ``log_unaries`` materialise the
+    reference's host arrays on demand.
+    """
+
+    def __init__(self, left: np.ndarray, right: np.ndarray, params: StereoParams, potential):
+        h, w = right.shape
+        self.M = int(params.M)
+        self.grid_shape = (int(h), int(w))
+        self.shared_potential = potential
+        self._edges = None
+        self._host = None
+        self._log_unaries = None
+        self.stereo_source = (left, right, float(params.beta), float(params.T_u))
+
+    def _materialise(self):
+        if self._host is None:
+            left, right, beta, T_u = self.stereo_source
+            u, lu = _unary_field(left, right, self.M, beta, T_u)
+            u.setflags(write=False)
+            lu.setflags(write=False)
+            self._host = (u, lu)
+        return self._host
+
+    @property
+    def unaries(self) -> np.ndarray:
+        return self._materialise()[0]
+
+    @property
+    def log_unaries(self) -> np.ndarray:
+        return self._materialise()[1]
+
+    @property
+    def n_nodes(self) -> int:
+        return self.grid_shape[0] * self.grid_shape[1]
+
+
+def build_stereo_mrf(left, right, params: StereoParams) -> StereoMrf:
+    """Reference stereo.py:128-140: shared truncated-linear smoothness
+    potential, unaries from the pair (built on the GPU by the engine)."""
+    L = _pixels(left)
+    R = _pixels(right)
+    if L.shape != R.shape:
+        raise ValueError(f"image dimensions differ: left {L.shape}, right {R.shape}")
+    if params.M > R.shape[1]:
+        raise ValueError(f"M={params.M} exceeds image width {R.shape[1]}")
+    pot = truncated_linear_potential(params.M, params.alpha, params.T_b)
+    return StereoMrf(np.ascontiguousarray(L), np.ascontiguousarray(R), params, pot)
+
+
+def disparity_to_image(labels, M: int, height: int, width: int) -> GrayImage:
+    """round(label * 255 / max(M-1, 1)), half up (reference stereo.py:143-154)."""
+    labels = np.asarray(labels)
+    if labels.size != height * width:
+        raise ValueError(f"expected {height * width} labels, got {labels.size}")
+    if labels.size and (labels.min() < 0 or labels.max() >= M):
+        raise ValueError(f"labels must lie in [0, {M})")
+    scaled = np.floor(labels.astype(np.float64) * (255.0 / max(M - 1, 1)) + 0.5)
+    return GrayImage(scaled.astype(np.uint8).reshape(height, width))
+
+
+def random_dot_pair(height: int, width: int, disparity, seed: int = 0, levels: int = 256):
+    left, right = _random_dot_pair(height, width, disparity, seed=seed, levels=levels)
+    return GrayImage(left), GrayImage(right)

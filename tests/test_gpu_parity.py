@@ -277,3 +277,23 @@ def test_rolled_and_unrolled_kernels_agree_bitwise(tmp_path, name, domain):
     a = _run_subprocess({"SBP_ROLL_MIN_R": "1"}, name, domain, 7, tmp_path / "a.npy")
     b = _run_subprocess({"SBP_ROLL_MIN_R": "99"}, name, domain, 7, tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_device_stereo_unaries(domain):
+    """build_stereo_mrf builds the unaries on the GPU from the image pair; they
+    equal the reference-formula host table (f64 -> f32), and BP on them
+    matches the oracle."""
+    from paper_1010_0012_b200.engine import GridEngine
+    left, right, _ = synth.noisy_stereo_pair(40, 72, 32, 5.0, 9)
+    params = sbp.StereoParams(M=32, alpha=0.5, T_b=3.0, beta=0.1, T_u=255.0)
+    model = sbp.build_stereo_mrf(left, right, params)
+    eng = GridEngine(model, domain, "fast")
+    host = model.unaries if domain == "sum" else model.log_unaries
+    if domain == "max":
+        host = host - host.max(axis=1, keepdims=True)
+    got = eng.values[:, :, :32].reshape(-1, 32).double().cpu().numpy()
+    want = host.astype(np.float32).astype(np.float64)
+    ulps = np.abs(got - want) / np.maximum(np.spacing(np.abs(want).astype(np.float32)), 1e-45)
+    assert ulps.max() <= 1.0          # f64 exp on the device vs numpy: <= 1 f32 ulp
+    check_run(model, 12, domain)
