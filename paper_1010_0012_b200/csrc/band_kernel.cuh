@@ -238,43 +238,13 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&
     if (!ok && j == 0) report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
 
-// One warp-group of PPW = 32/LP nodes (flattened pixel group `grp`).
+// The four messages of one node from its unary and incoming vectors.
 template <int DOM, int VL, int LP, int R>
-__device__ __forceinline__ void band_group(const BandArgs &a, long long grp, long long npix) {
-    constexpr int PPW = 32 / LP;
-    const int lane = threadIdx.x & 31;
-    const int j = lane % LP;
-    long long p = grp * PPW + lane / LP;
-    const bool valid = p < npix;
-    if (!valid) p = npix - 1;
-    const int lr = a.lr_begin + (int)(p / a.W);
-    const int c = (int)(p % a.W);
-    const long long r = (long long)a.r0 + lr - 1;
-    const long long node_l = (long long)lr * a.W + c;
-    const int x0 = j * VL;
-
-    float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
-    Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
-    const float *mi = a.msgs_in + node_l * a.Ms + x0;
-    if (!a.first) {
-        Vec8Loader<VL>::load(m0, mi);
-        Vec8Loader<VL>::load(m1, mi + a.slot_stride);
-        Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
-        Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
-    } else {
-        // bp.py:587-601 without touching memory: 1/M on real slots, the
-        // identity on ghost slots, padding 0 / -inf
-        const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
-        float *mm[4] = {m0, m1, m2, m3};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
-#pragma unroll
-            for (int i = 0; i < VL; ++i)
-                mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
-        }
-    }
-
+__device__ __forceinline__ void band_group_body(const BandArgs &a, const float (&g)[VL],
+                                                const float (&m0)[VL], const float (&m1)[VL],
+                                                const float (&m2)[VL], const float (&m3)[VL],
+                                                int j, int x0, bool valid, long long node_l,
+                                                long long r, int c) {
     const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
     float h[VL];
     if (DOM == SBP_SUM) {
@@ -360,6 +330,46 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
             emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     }
+}
+
+// One warp-group of PPW = 32/LP nodes (flattened pixel group `grp`).
+template <int DOM, int VL, int LP, int R>
+__device__ __forceinline__ void band_group(const BandArgs &a, long long grp, long long npix) {
+    constexpr int PPW = 32 / LP;
+    const int lane = threadIdx.x & 31;
+    const int j = lane % LP;
+    long long p = grp * PPW + lane / LP;
+    const bool valid = p < npix;
+    if (!valid) p = npix - 1;
+    const int lr = a.lr_begin + (int)(p / a.W);
+    const int c = (int)(p % a.W);
+    const long long r = (long long)a.r0 + lr - 1;
+    const long long node_l = (long long)lr * a.W + c;
+    const int x0 = j * VL;
+
+    float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
+    Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
+    const float *mi = a.msgs_in + node_l * a.Ms + x0;
+    if (!a.first) {
+        Vec8Loader<VL>::load(m0, mi);
+        Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+        Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+        Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+    } else {
+        // bp.py:587-601 without touching memory: 1/M on real slots, the
+        // identity on ghost slots, padding 0 / -inf
+        const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+        float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+        }
+    }
+
+    band_group_body<DOM, VL, LP, R>(a, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
 }
 
 // Rolled variant for potentials whose two orientations carry the same band
@@ -456,6 +466,158 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, long long g
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant: each warp double-buffers its pixel groups in shared
+// memory with 1-D bulk copies (cp.async.bulk, completion on an mbarrier), so
+// the next group's five input vectors are always in flight while the current
+// one is computed -- memory-level parallelism without extra registers.
+// ---------------------------------------------------------------------------
+constexpr int STG_WARPS = 4;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    }
+}
+
+template <int DOM, int VL, int LP, int R>
+__global__ void __launch_bounds__(32 * STG_WARPS)
+band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
+    constexpr int PPW = 32 / LP;
+    constexpr int VEC = 32 * VL;                 // floats of one vector for one group
+    extern __shared__ __align__(128) float stg_smem[];
+    __shared__ __align__(8) unsigned long long bars[STG_WARPS][2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = lane % LP, q = lane / LP;
+    const int x0 = j * VL;
+    float *buf = stg_smem + warp * (2 * 5 * VEC);
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long ngroups = (npix + PPW - 1) / PPW;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0) {
+        mbar_init(&bars[warp][0], 1);
+        mbar_init(&bars[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int nvec = a.first ? 1 : 5;
+    auto issue = [&](long long g, int st) {
+        if (lane == 0) {
+            const long long p0 = g * PPW;
+            const long long n = npix - p0 < PPW ? npix - p0 : PPW;
+            const unsigned bytes = (unsigned)(n * a.Ms * 4);
+            float *dst = buf + st * 5 * VEC;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bars[warp][st], bytes * nvec);
+            bulk_g2s(dst, a.values + ((long long)(a.lr_begin - 1) * a.W + p0) * a.Ms, bytes,
+                     &bars[warp][st]);
+            if (!a.first)
+                for (int k = 0; k < 4; ++k)
+                    bulk_g2s(dst + (1 + k) * VEC,
+                             a.msgs_in + k * a.slot_stride + ((long long)a.lr_begin * a.W + p0) * a.Ms,
+                             bytes, &bars[warp][st]);
+        }
+    };
+    unsigned phase = 0;   // bit st: parity of stage st
+    int st = 0;
+    if (grp < ngroups) issue(grp, 0);
+    for (; grp < ngroups; grp += nwarps) {
+        if (grp + nwarps < ngroups) issue(grp + nwarps, st ^ 1);
+        mbar_wait(&bars[warp][st], (phase >> st) & 1);
+        phase ^= 1u << st;
+        long long p = grp * PPW + q;
+        const bool valid = p < npix;
+        if (!valid) p = npix - 1;
+        const int lr = a.lr_begin + (int)(p / a.W);
+        const int c = (int)(p % a.W);
+        const long long r = (long long)a.r0 + lr - 1;
+        const long long node_l = (long long)lr * a.W + c;
+        const float *src = buf + st * 5 * VEC + q * a.Ms + x0;
+        float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
+#pragma unroll
+        for (int i = 0; i < VL; i += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(src + i);
+            g[i] = v.x; g[i + 1] = v.y; g[i + 2] = v.z; g[i + 3] = v.w;
+        }
+        if (!a.first) {
+            float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int i = 0; i < VL; i += 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(src + (1 + k) * VEC + i);
+                    mm[k][i] = v.x; mm[k][i + 1] = v.y; mm[k][i + 2] = v.z; mm[k][i + 3] = v.w;
+                }
+        } else {
+            const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+            float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
+#pragma unroll
+                for (int i = 0; i < VL; ++i)
+                    mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+            }
+        }
+        __syncwarp();   // every lane has read stage st before it is refilled
+        band_group_body<DOM, VL, LP, R>(a, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
+        st ^= 1;
+    }
+}
+
+template <int DOM, int VL, int LP, int R>
+cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
+    constexpr int PPW = 32 / LP;
+    const size_t smem = (size_t)STG_WARPS * 2 * 5 * 32 * VL * sizeof(float);
+    static int resident = 0, sms = 0;
+    if (!resident) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(band_iter_staged_kernel<DOM, VL, LP, R>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &resident, band_iter_staged_kernel<DOM, VL, LP, R>, 32 * STG_WARPS, smem);
+        if (resident < 1) resident = 1;
+    }
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long warps = (npix + PPW - 1) / PPW;
+    long long blocks = (warps + STG_WARPS - 1) / STG_WARPS;
+    if (blocks <= 0) return cudaSuccess;
+    const long long cap = (long long)sms * resident;
+    if (blocks > cap) blocks = cap;
+    band_iter_staged_kernel<DOM, VL, LP, R><<<(unsigned)blocks, 32 * STG_WARPS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 // L2 prefetch of one pixel group's five input vectors (unary + 4 incoming
 // slots).  node_l and the value index are linear in the flattened pixel
 // index, so each vector of a group is one contiguous chunk.
@@ -546,8 +708,33 @@ BandLaunchFn pick_band_r(int R) {
 
 // VL = 16 is compiled only where the sweeps chose it (sum, Ms >= 128); the
 // max domain always runs VL = 8 (its TwoSum state spills at VL = 16).
+template <int MS, int DOM, int VL>
+BandLaunchFn pick_band_staged_r(int R) {
+    if constexpr (VL > MS) {
+        return nullptr;
+    } else {
+        switch (R) {
+#define SBP_CASE(RR)                                                      \
+    case RR:                                                              \
+        if constexpr (RR < MS && RR <= 16)                                \
+            return &launch_band_staged<DOM, VL, MS / VL, RR>;             \
+        else return nullptr;
+            SBP_BAND_RADII(SBP_CASE)
+#undef SBP_CASE
+        default: return nullptr;
+        }
+    }
+}
+
+// rolled: 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged unrolled (R <= 16)
 template <int MS, int DOM>
 BandLaunchFn pick_band_dom(int vl, int R, int rolled) {
+    if (rolled == 2) {
+        if (vl == 8) return pick_band_staged_r<MS, DOM, 8>(R);
+        if constexpr (DOM == SBP_SUM && MS >= 128)
+            if (vl == 16) return pick_band_staged_r<MS, DOM, 16>(R);
+        return nullptr;
+    }
     if (vl == 8) return rolled ? pick_band_r<MS, DOM, 8, true>(R) : pick_band_r<MS, DOM, 8, false>(R);
     if constexpr (DOM == SBP_SUM && MS >= 128) {
         if (vl == 16)

@@ -60,6 +60,15 @@ int band_prefetch() {
     return v;
 }
 
+int band_staged() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBP_STAGED");
+        v = e ? atoi(e) != 0 : 0;
+    }
+    return v;
+}
+
 int band_vl(int Ms, int domain) {
     if (const char *e = getenv("SBP_BAND_VL")) {
         int v = atoi(e);
@@ -158,7 +167,8 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
             sym = pot->band_w[0][k] == pot->band_w[1][k] ||
                   (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
-        const int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;   // compiled for R >= 24
+        int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;   // compiled for R >= 24
+        if (!rolled && band_staged() && Rk <= 16) rolled = 2;          // TMA-staged variant
         sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk, rolled) : nullptr;
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
@@ -279,9 +289,11 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
             for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
                 sym = pot->band_w[0][k] == pot->band_w[1][k] ||
                       (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
-            const int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;
-            snprintf(buf, len, "band_iter_kernel<%s,VL=%d,LP=%d,R=%d,%s>", dom, vl, g->Ms / vl, Rk,
-                     rolled ? "rolled" : "unrolled");
+            int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;
+            if (!rolled && band_staged() && Rk <= 16) rolled = 2;
+            snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
+                     rolled == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom, vl,
+                     g->Ms / vl, Rk, rolled == 1 ? ",rolled" : "");
         }
     } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
         snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
