@@ -696,7 +696,8 @@ BandLaunchFn pick_band_r(int R) {
         switch (R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
-        if constexpr (RR < MS && (!ROLLED || RR >= 24))                   \
+        if constexpr (RR < MS && (!ROLLED || RR >= 24) &&                   \
+                      (VL == 8 || ROLLED || RR <= 3))                         \
             return &launch_band<DOM, VL, MS / VL, RR, ROLLED>;             \
         else return nullptr;
             SBP_BAND_RADII(SBP_CASE)
@@ -729,12 +730,7 @@ BandLaunchFn pick_band_staged_r(int R) {
 // rolled: 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged unrolled (R <= 16)
 template <int MS, int DOM>
 BandLaunchFn pick_band_dom(int vl, int R, int rolled) {
-    if (rolled == 2) {
-        if (vl == 8) return pick_band_staged_r<MS, DOM, 8>(R);
-        if constexpr (DOM == SBP_SUM && MS >= 128)
-            if (vl == 16) return pick_band_staged_r<MS, DOM, 16>(R);
-        return nullptr;
-    }
+    if (rolled == 2) return vl == 8 ? pick_band_staged_r<MS, DOM, 8>(R) : nullptr;
     if (vl == 8) return rolled ? pick_band_r<MS, DOM, 8, true>(R) : pick_band_r<MS, DOM, 8, false>(R);
     if constexpr (DOM == SBP_SUM && MS >= 128) {
         if (vl == 16)

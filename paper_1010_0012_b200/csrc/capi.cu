@@ -60,34 +60,48 @@ int band_prefetch() {
     return v;
 }
 
-int band_staged() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBP_STAGED");
-        v = e ? atoi(e) != 0 : 0;
-    }
-    return v;
+// Band kernel variant choice, from the B200 A/B runs (tools/ab_vl.sh,
+// tools/ab_staged.sh; profiles/r01_kernel_variants.md).  Environment
+// overrides: SBP_BAND_VL=8|16, SBP_STAGED=0|1, SBP_ROLL_MIN_R=<r>.
+int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
 }
 
-int band_vl(int Ms, int domain) {
-    if (const char *e = getenv("SBP_BAND_VL")) {
-        int v = atoi(e);
-        if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128)) return v;
-    }
-    // B200 A/B (tools/ab_vl.sh): at Ms = 128 VL = 8 is 1.6 % faster per cold
-    // launch but VL = 16 (fewer shuffles per label, less power) holds ~5 %
-    // better under the sustained power cap; max-sum always VL = 8
-    return (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
-}
+struct BandChoice {
+    int vl;       // labels per lane
+    int variant;  // 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged (R <= 16)
+};
 
-// Rolled (single band copy) kernel for symmetric potentials with R >= this.
 int band_roll_min_r() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBP_ROLL_MIN_R");
-        v = e ? atoi(e) : 24;   // sweep (tools/sweep_r01b.sh): wins at R = 32, loses at R <= 16
-    }
+    static int v = env_int("SBP_ROLL_MIN_R", 24);   // rolled wins at R = 32, loses at R <= 16
     return v;
+}
+
+BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
+    BandChoice c;
+    if (sym && Rk >= 24 && Rk >= band_roll_min_r()) {
+        c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
+        c.variant = 1;
+    } else {
+        // staged VL=8: +7 % on C3 max, +2.5 % on C5 T=9 sum, ~= VL=16 on C4 sum;
+        // plain VL=16 wins for the lightest band (C5 T=2: R=1 at Ms=256)
+        const bool staged_default = domain == SBP_MAX || Ms <= 128 || Rk >= 4;
+        const int staged = env_int("SBP_STAGED", staged_default ? 1 : 0) && Rk <= 16;
+        c.variant = staged ? 2 : 0;
+        c.vl = staged ? 8 : ((domain == SBP_SUM && Ms >= 128) ? 16 : 8);
+    }
+    const int v = env_int("SBP_BAND_VL", 0);
+    if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128 && c.variant != 2)) c.vl = v;
+    return c;
+}
+
+bool band_symmetric(const sbp_potential *pot) {
+    bool sym = pot->fbar[0] == pot->fbar[1];
+    for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
+        sym = pot->band_w[0][k] == pot->band_w[1][k] ||
+              (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
+    return sym;
 }
 
 sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled) {
@@ -162,14 +176,9 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         int Rk = 0;
         for (int r : kRadii)
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
-        const int vl = band_vl(g->Ms, pot->domain);
-        bool sym = pot->fbar[0] == pot->fbar[1];
-        for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
-            sym = pot->band_w[0][k] == pot->band_w[1][k] ||
-                  (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
-        int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;   // compiled for R >= 24
-        if (!rolled && band_staged() && Rk <= 16) rolled = 2;          // TMA-staged variant
-        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, vl, Rk, rolled) : nullptr;
+        const BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
+        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, ch.vl, Rk, ch.variant) : nullptr;
+        if (!fn && Rk) fn = band_fn(g->Ms, pot->domain, 8, Rk, 0);   // always compiled
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
         sbp::BandArgs a;
@@ -284,16 +293,10 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         if (sequential) {
             snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
         } else {
-            const int vl = band_vl(g->Ms, pot->domain);
-            bool sym = pot->fbar[0] == pot->fbar[1];
-            for (int k = 0; k < 2 * pot->R + 1 && sym; ++k)
-                sym = pot->band_w[0][k] == pot->band_w[1][k] ||
-                      (pot->band_w[0][k] != pot->band_w[0][k] && pot->band_w[1][k] != pot->band_w[1][k]);
-            int rolled = sym && Rk >= band_roll_min_r() && Rk >= 24;
-            if (!rolled && band_staged() && Rk <= 16) rolled = 2;
+            const BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
             snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
-                     rolled == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom, vl,
-                     g->Ms / vl, Rk, rolled == 1 ? ",rolled" : "");
+                     ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom, ch.vl,
+                     g->Ms / ch.vl, Rk, ch.variant == 1 ? ",rolled" : "");
         }
     } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
         snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
