@@ -297,7 +297,7 @@ def run_ours(args, cfg):
     # e2e through the public API with host buffers (rank 0 at N=1 only)
     e2e = None
     cpu = None
-    if world == 1:
+    if world == 1 and not args.kernel_only:
         e2e = e2e_public_api(args, cfg, torch)
         ups, cores, sample = cpu_sample(cfg, args.domain)
         cpu = {"value": ups, "unit": "updates/s", "cores": cores, "kind": "port",
@@ -402,6 +402,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--domain", default=None)
     ap.add_argument("--iters", type=int, default=None)
+    ap.add_argument("--kernel-only", action="store_true",
+                    help="skip the e2e and CPU-baseline legs (kernel A/B runs)")
     args = ap.parse_args()
     from paper_1010_0012_b200 import synth
     cfg = synth.CONFIGS[args.config]

@@ -274,8 +274,12 @@ def _run_subprocess(env_extra, name, domain, iters, out):
 
 @pytest.mark.parametrize("name,domain", [("C4", "sum"), ("C3", "max"), ("C5_T33", "sum")])
 def test_rolled_and_unrolled_kernels_agree_bitwise(tmp_path, name, domain):
-    a = _run_subprocess({"SBP_ROLL_MIN_R": "1"}, name, domain, 7, tmp_path / "a.npy")
-    b = _run_subprocess({"SBP_ROLL_MIN_R": "99"}, name, domain, 7, tmp_path / "b.npy")
+    """The rolled (one band copy) and unrolled kernels perform identical arithmetic."""
+    # same lane width (VL=8) so both variants use the same reduction trees
+    a = _run_subprocess({"SBP_ROLL_MIN_R": "1", "SBP_BAND_VL": "8", "SBP_STAGED": "0"},
+                        name, domain, 7, tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_ROLL_MIN_R": "99", "SBP_BAND_VL": "8", "SBP_STAGED": "0"},
+                        name, domain, 7, tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
 
 
@@ -297,3 +301,14 @@ def test_device_stereo_unaries(domain):
     ulps = np.abs(got - want) / np.maximum(np.spacing(np.abs(want).astype(np.float32)), 1e-45)
     assert ulps.max() <= 1.0          # f64 exp on the device vs numpy: <= 1 f32 ulp
     check_run(model, 12, domain)
+
+
+
+@pytest.mark.parametrize("name,domain", [("C4", "sum"), ("C3", "max"), ("C5_T9", "sum")])
+def test_staged_and_register_kernels_agree_bitwise(tmp_path, name, domain):
+    """The TMA-staged variant only changes how inputs reach the registers."""
+    a = _run_subprocess({"SBP_STAGED": "1", "SBP_BAND_VL": "8"}, name, domain, 7,
+                        tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_STAGED": "0", "SBP_BAND_VL": "8"}, name, domain, 7,
+                        tmp_path / "b.npy")
+    np.testing.assert_array_equal(a, b)
