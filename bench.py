@@ -111,6 +111,27 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def sustained_copy_gbs(torch, dev, seconds: float = 2.0) -> float:
+    """Copy bandwidth (read + write bytes) held for `seconds` of back-to-back
+    1 GiB device copies -- the same sustained, power-capped regime as the
+    timed message kernels (MEASURED_PEAKS.json holds a best-of-10 burst)."""
+    a = torch.empty(1 << 29, dtype=torch.float16, device=dev)
+    b = torch.empty_like(a)
+    b.copy_(a)
+    torch.cuda.synchronize()
+    n, t0 = 0, time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(20):
+            b.copy_(a)
+        n += 20
+        torch.cuda.synchronize()
+    ev1.record()
+    torch.cuda.synchronize()
+    return 2 * a.numel() * a.element_size() * n / (ev0.elapsed_time(ev1) / 1e3) / 1e9
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -286,6 +307,7 @@ def run_ours(args, cfg):
     kern_ms = sum(a.elapsed_time(b) for a, b, n in iter_events) / max(
         1, sum(n for _, _, n in iter_events))
 
+    sus = sustained_copy_gbs(torch, dev) if rank == 0 else None
     E = cfg.n_directed
     value = E * args.iters * args.steps / (ms / 1e3)
     pot = smodel.shared_potential
@@ -315,7 +337,9 @@ def run_ours(args, cfg):
                      "peak_source": peak_src, "kernel": eng.kernel_name,
                      "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": B / world,
                      "flops_per_launch": F / world,
-                     "fp32_frac_nominal": (F / world) / (kern_ms / 1e3) / 1e12 / FP32_NOMINAL_TFLOPS},
+                     "fp32_frac_nominal": (F / world) / (kern_ms / 1e3) / 1e12 / FP32_NOMINAL_TFLOPS,
+                     "sustained_copy_gbs": sus,
+                     "frac_of_sustained_copy": achieved / sus if sus else None},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
