@@ -58,7 +58,7 @@ def algorithmic(cfg, pot):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks.mem,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -95,19 +95,22 @@ class ClockSampler:
         rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) != 6:
+            if len(parts) != 8:
                 continue
             try:
-                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+                rows.append((float(parts[0]), float(parts[1]), parts[4:], float(parts[2]),
+                             float(parts[3])))
             except ValueError:
                 continue
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r)
+        reasons = sorted({names[i] for _, _, r, _, _ in rows for i, v in enumerate(r)
                           if v.lower() == "active"})
         return {"sm_mhz": float(np.median([r[0] for r in rows])),
                 "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "mem_mhz": float(np.median([r[3] for r in rows])),
+                "power_w": float(np.median([r[4] for r in rows])),
                 "samples": len(rows)}
 
 
@@ -333,7 +336,7 @@ def run_ours(args, cfg):
         "data": "synthetic (seeded random-dot stereo, 8-rectangle disparity, sigma=5 noise)",
         "config": config_dict(cfg, args, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic_for("band_iter_kernel"),
+                     "frac": achieved / hbm_peak, "traffic": traffic_for(eng.kernel_name.split("<")[0]),
                      "peak_source": peak_src, "kernel": eng.kernel_name,
                      "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": B / world,
                      "flops_per_launch": F / world,
