@@ -80,12 +80,21 @@ typedef struct {
     int m_max;           /* ELL: entries per column */
     float fbar[2];       /* per orientation: fbar (sum) or ln fbar (max) */
     float band_w[2][2 * SBP_MAX_R + 1];   /* BAND: w[o][d + R] (residual | log value) */
-    const int32_t *ell_idx[2];            /* ELL: device [m_max][Ms], x_i per (k, x_j) */
-    const float *ell_w[2];                /* ELL: device [m_max][Ms] */
+    const int32_t *ell_idx[2];            /* ELL: device [m_max][Ms] per orientation, x_i per
+                                             (k, x_j); ell_idx[1] == ell_idx[0] + m_max*Ms */
+    const float *ell_w[2];                /* ELL: device [m_max][Ms], same layout */
     const float *dense_t[2];              /* DENSE: device [Ms][Ms] per orientation,
                                              f(x_i = k, x_j = x) at [k][x] (tiled kernel,
                                              Ms >= 32); smaller Ms runs the ELL arrays with
                                              m_max = M, idx[k][x] = k */
+    /* ELL per-edge (inhomogeneous) potentials, n_pot > 0: ell_idx[0] / ell_w[0]
+     * point at [n_pot][2][m_max][Ms], fbar_all at [n_pot][2]; pid_h[r*W + c]
+     * is the potential of edge (n, n+1), pid_v[r*W + c] of edge (n, n+W)
+     * (global node n = r*W + c).  n_pot = 0: one shared potential. */
+    int n_pot;
+    const float *fbar_all;
+    const int32_t *pid_h;
+    const int32_t *pid_v;
 } sbp_potential;
 
 SBP_API int sbp_version(void);
@@ -121,9 +130,11 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
 
 /* One canonical SEQUENTIAL sweep in place (the reference's default schedule,
  * bp.py:492-503 -> numba_kernels.py:274-407): passes L->R, R->L, T->B, B->T,
- * each a set of independent row / column chains updated in order.  Full grid,
- * band potentials.  Failures: err = min(sweep << 40 | pass << 38 |
- * line * line_len + position), i.e. the reference's first failing message. */
+ * each a set of independent row / column chains updated in order.  Full grid.
+ * Failures: err = min(sweep << 40 | pass << 38 |
+ * line * line_len + position), i.e. the reference's first failing message.
+ * Band potentials run the chain kernels; ELL / per-edge / dense potentials a
+ * warp-per-chain ELL kernel. */
 SBP_API int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values,
                       float *msgs, int sweep, unsigned long long *err, void *stream);
 

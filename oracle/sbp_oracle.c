@@ -200,18 +200,30 @@ void oracle_init_msgs(double *msgs, int H, int W, int M, int r0, int rows, int d
         }
 }
 
+/* Potential of the message node (r, c) -> direction dir: shared (pid arrays
+ * NULL: pots[orientation]) or per edge (pots[2 * pid + orientation], pid_h[n]
+ * for edge (n, n+1), pid_v[n] for (n, n+W); reference _GenericEngine opid,
+ * bp.py:516-525). */
+static const oracle_pot *pot_of(const oracle_pot *pots, const int *pid_h, const int *pid_v,
+                                int64_t W, int64_t r, int64_t c, int dir) {
+    int64_t pid = 0;
+    if (pid_h) {
+        int64_t n = r * W + c;
+        pid = dir == 0 ? pid_h[n] : dir == 1 ? pid_h[n - 1] : dir == 2 ? pid_v[n] : pid_v[n - W];
+    }
+    return &pots[2 * pid + DIR_ORIENT[dir]];
+}
+
 /* One synchronous iteration over local rows [lr_begin, lr_end).
  * msgs_out must already hold the ghost/identity values (it is never written
  * at ghost slots).  Returns -1, or the smallest reference directed-edge id
  * whose message could not be normalised. */
-int64_t oracle_sync_iterate(int H, int W, int M, int r0, int rows, int lr_begin, int lr_end,
-                            int domain, int kernel, const double *unary,
-                            const double *msgs_in, double *msgs_out,
-                            const oracle_pot *pot0, const oracle_pot *pot1, int nthreads) {
+int64_t oracle_sync_iterate_pe(int H, int W, int M, int r0, int rows, int lr_begin, int lr_end,
+                               int domain, int kernel, const double *unary,
+                               const double *msgs_in, double *msgs_out, const oracle_pot *pots,
+                               const int *pid_h, const int *pid_v, int nthreads) {
     int64_t slot = (int64_t)(rows + 2) * W * M;
     int64_t fail = INT64_MAX;
-    const oracle_pot *pots[2] = {pot0, pot1};
-    (void)rows;
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads) reduction(min : fail)
     for (int lr = lr_begin; lr < lr_end; ++lr) {
         double *h = (double *)malloc(sizeof(double) * 2 * M);
@@ -227,7 +239,7 @@ int64_t oracle_sync_iterate(int H, int W, int M, int r0, int rows, int lr_begin,
                 if (!exists) continue;
                 int64_t step = dir == 0 ? 1 : dir == 1 ? -1 : dir == 2 ? W : -W;
                 grid_h(g, m, DIR_EXCL[dir], h, M, domain);
-                apply_kernel(kernel, domain, h, pots[DIR_ORIENT[dir]], out, M);
+                apply_kernel(kernel, domain, h, pot_of(pots, pid_h, pid_v, W, r, c, dir), out, M);
                 double *dst = msgs_out + DIR_WSLOT[dir] * slot + (ln + step) * M;
                 if (!norm_store(out, dst, M, domain)) {
                     int64_t id = oracle_directed_edge_id(H, W, r, c, dir);
@@ -240,16 +252,24 @@ int64_t oracle_sync_iterate(int H, int W, int M, int r0, int rows, int lr_begin,
     return fail == INT64_MAX ? -1 : fail;
 }
 
+int64_t oracle_sync_iterate(int H, int W, int M, int r0, int rows, int lr_begin, int lr_end,
+                            int domain, int kernel, const double *unary,
+                            const double *msgs_in, double *msgs_out,
+                            const oracle_pot *pot0, const oracle_pot *pot1, int nthreads) {
+    oracle_pot pots[2] = {*pot0, *pot1};
+    return oracle_sync_iterate_pe(H, W, M, r0, rows, lr_begin, lr_end, domain, kernel, unary,
+                                  msgs_in, msgs_out, pots, NULL, NULL, nthreads);
+}
+
 /* One canonical sequential sweep (bp.py:492-503 `_run_grid`): passes
  * L->R, R->L, T->B, B->T, each an in-place chain (grid_pass_*,
  * numba_kernels.py:274-407).  msgs4 is the reference (4, N, M) layout without
  * halo rows.  Returns -1 or the failing flat source node; *fail_dir receives
  * the pass direction.  *madds accumulates the reference madd counter. */
-int64_t oracle_seq_sweep(int H, int W, int M, int domain, int kernel, const double *values_in,
-                         double *msgs4, const oracle_pot *pot0, const oracle_pot *pot1,
-                         int *fail_dir, int64_t *madds) {
+int64_t oracle_seq_sweep_pe(int H, int W, int M, int domain, int kernel,
+                            const double *values_in, double *msgs4, const oracle_pot *pots,
+                            const int *pid_h, const int *pid_v, int *fail_dir, int64_t *madds) {
     int64_t N = (int64_t)H * W;
-    const oracle_pot *pots[2] = {pot0, pot1};
     double *h = (double *)malloc(sizeof(double) * 2 * M);
     double *out = h + M;
     int64_t ret = -1;
@@ -259,9 +279,6 @@ int64_t oracle_seq_sweep(int H, int W, int M, int domain, int kernel, const doub
         else if (dir == 1) { n_lines = H; line_len = W - 1; line_stride = W; step = -1; origin = W - 1; }
         else if (dir == 2) { n_lines = W; line_len = H - 1; line_stride = 1; step = W; origin = 0; }
         else { n_lines = W; line_len = H - 1; line_stride = 1; step = -W; origin = (int64_t)(H - 1) * W; }
-        const oracle_pot *p = pots[DIR_ORIENT[dir]];
-        int64_t per = kernel == K_STANDARD ? (int64_t)M * M
-                    : kernel == K_FAST ? p->indptr[M] + 2 * (int64_t)M : p->indptr[M];
         int64_t done = 0;
         for (int64_t line = 0; line < n_lines && ret < 0; ++line) {
             int64_t base = line * line_stride + origin;
@@ -269,9 +286,13 @@ int64_t oracle_seq_sweep(int H, int W, int M, int domain, int kernel, const doub
                 int64_t src = base + pos * step;
                 const double *m[4];
                 for (int k = 0; k < 4; ++k) m[k] = msgs4 + k * N * M + src * M;
+                const oracle_pot *p = pot_of(pots, pid_h, pid_v, W, src / W, src % W, dir);
                 grid_h(values_in + src * M, m, DIR_EXCL[dir], h, M, domain);
                 apply_kernel(kernel, domain, h, p, out, M);
                 ++done;
+                *madds += kernel == K_STANDARD ? (int64_t)M * M
+                        : kernel == K_FAST ? p->indptr[M] - p->indptr[0] + 2 * (int64_t)M
+                                           : p->indptr[M] - p->indptr[0];
                 if (!norm_store(out, msgs4 + DIR_WSLOT[dir] * N * M + (src + step) * M, M,
                                 domain)) {
                     ret = src;
@@ -280,10 +301,18 @@ int64_t oracle_seq_sweep(int H, int W, int M, int domain, int kernel, const doub
                 }
             }
         }
-        *madds += per * done;
+        (void)done;
     }
     free(h);
     return ret;
+}
+
+int64_t oracle_seq_sweep(int H, int W, int M, int domain, int kernel, const double *values_in,
+                         double *msgs4, const oracle_pot *pot0, const oracle_pot *pot1,
+                         int *fail_dir, int64_t *madds) {
+    oracle_pot pots[2] = {*pot0, *pot1};
+    return oracle_seq_sweep_pe(H, W, M, domain, kernel, values_in, msgs4, pots, NULL, NULL,
+                               fail_dir, madds);
 }
 
 /* max |a-b| over n entries (reference convergence test, bp.py:671-676). */

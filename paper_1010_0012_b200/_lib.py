@@ -31,7 +31,9 @@ class SbpPotential(ctypes.Structure):
                 ("fbar", ctypes.c_float * 2),
                 ("band_w", (ctypes.c_float * (2 * SBP_MAX_R + 1)) * 2),
                 ("ell_idx", ctypes.c_void_p * 2), ("ell_w", ctypes.c_void_p * 2),
-                ("dense_t", ctypes.c_void_p * 2)]
+                ("dense_t", ctypes.c_void_p * 2),
+                ("n_pot", ctypes.c_int), ("fbar_all", ctypes.c_void_p),
+                ("pid_h", ctypes.c_void_p), ("pid_v", ctypes.c_void_p)]
 
 
 class SbpError(RuntimeError):

@@ -25,12 +25,16 @@ struct EllArgs {
     unsigned long long *err;
     long long slot_stride;
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term, m_max;
-    int first;
-    float fbar[2];
-    const int *idx[2];
-    const float *w[2];
+    int first, pass;
+    float fbar[2];              // shared potential: per orientation
+    const int *idx;             // [n_pot][2][m_max][Ms]
+    const float *w;             // [n_pot][2][m_max][Ms]
+    long long pot_stride;       // m_max * Ms
+    const float *fbar_all;      // per-edge: [n_pot][2], else NULL
+    const int *pid_h, *pid_v;   // per-edge potential ids (global nodes), else NULL
 };
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s);
+cudaError_t launch_ell_sweep(int domain, const EllArgs &a, cudaStream_t s);
 
 struct DenseArgs {
     const float *values;

@@ -116,6 +116,34 @@ sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled) {
     }
 }
 
+int ell_args(const sbp_grid *g, const sbp_potential *pot, sbp::EllArgs *a) {
+    memset(a, 0, sizeof *a);
+    if (pot->m_max < 1 || !pot->ell_idx[0] || !pot->ell_w[0])
+        return fail(SBP_EINVAL, "ELL potential arrays missing");
+    const long long ps = (long long)pot->m_max * g->Ms;
+    if (pot->n_pot == 0) {
+        if (pot->ell_idx[1] != pot->ell_idx[0] + ps || pot->ell_w[1] != pot->ell_w[0] + ps)
+            return fail(SBP_EINVAL, "ELL orientation 1 must follow orientation 0 contiguously");
+    } else if (!pot->fbar_all || !pot->pid_h || !pot->pid_v) {
+        return fail(SBP_EINVAL, "per-edge ELL potential needs fbar_all, pid_h and pid_v");
+    }
+    a->slot_stride = (long long)(g->rows + 2) * g->W * g->Ms;
+    a->H = g->H; a->W = g->W; a->M = g->M; a->Ms = g->Ms; a->r0 = g->r0;
+    a->floor_term = pot->kind == SBP_POT_DENSE ? 0 : pot->floor_term;
+    a->m_max = pot->m_max;
+    a->fbar[0] = pot->fbar[0];
+    a->fbar[1] = pot->fbar[1];
+    a->idx = pot->ell_idx[0];
+    a->w = pot->ell_w[0];
+    a->pot_stride = ps;
+    if (pot->n_pot > 0) {
+        a->fbar_all = pot->fbar_all;
+        a->pid_h = pot->pid_h;
+        a->pid_v = pot->pid_v;
+    }
+    return SBP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -200,7 +228,8 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         }
         return cuda_status(fn(a, s), "sbp_iterate(band)");
     }
-    if (pot->kind == SBP_POT_DENSE && pot->dense_t[0] && pot->dense_t[1] && g->Ms >= 32) {
+    if (pot->kind == SBP_POT_DENSE && pot->n_pot == 0 && pot->dense_t[0] && pot->dense_t[1] &&
+        g->Ms >= 32) {
         sbp::DenseArgs a;
         a.values = values;
         a.msgs_in = msgs_in;
@@ -215,25 +244,14 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         return cuda_status(sbp::launch_dense(pot->domain, a, s), "sbp_iterate(dense)");
     }
     if (pot->kind == SBP_POT_ELL || pot->kind == SBP_POT_DENSE) {
-        if (pot->m_max < 0 || !pot->ell_idx[0] || !pot->ell_idx[1] || !pot->ell_w[0] ||
-            !pot->ell_w[1])
-            return fail(SBP_EINVAL, "ELL potential arrays missing");
         sbp::EllArgs a;
+        if (int rc = ell_args(g, pot, &a)) return rc;
         a.values = values;
         a.msgs_in = msgs_in;
         a.msgs_out = msgs_out;
         a.err = err;
-        a.slot_stride = slot;
-        a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
-        a.floor_term = pot->kind == SBP_POT_DENSE ? 0 : pot->floor_term;
-        a.m_max = pot->m_max;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
-        for (int o = 0; o < 2; ++o) {
-            a.fbar[o] = pot->fbar[o];
-            a.idx[o] = pot->ell_idx[o];
-            a.w[o] = pot->ell_w[o];
-        }
         return cuda_status(sbp::launch_ell(pot->domain, a, s), "sbp_iterate(ell)");
     }
     return fail(SBP_EINVAL, "unknown potential kind %d", pot->kind);
@@ -244,10 +262,19 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
     if (int rc = check_grid(g)) return rc;
     if (!pot || !values || !msgs || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "sequential sweeps need the full grid");
-    if (pot->kind != SBP_POT_BAND)
-        return fail(SBP_EUNSUPPORTED, "sequential sweeps support band potentials only");
-    if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
     if (sweep < 0 || sweep >= (1 << 23)) return fail(SBP_EINVAL, "bad sweep index");
+    if (pot->kind != SBP_POT_BAND) {
+        sbp::EllArgs a;
+        if (int rc = ell_args(g, pot, &a)) return rc;
+        a.values = values;
+        a.msgs_in = msgs;
+        a.msgs_out = msgs;
+        a.err = err;
+        a.lr_begin = 1; a.lr_end = g->H + 1; a.iteration = sweep;
+        return cuda_status(sbp::launch_ell_sweep(pot->domain, a, (cudaStream_t)stream),
+                           "sbp_sweep(ell)");
+    }
+    if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
     int Rk = 0;
     for (int r : kRadii)
         if (r >= pot->R && r < g->Ms) { Rk = r; break; }

@@ -1,12 +1,22 @@
-// General-potential iteration: per-column compatible lists in ELL form.
+// General potentials: per-column compatible lists in ELL form, shared or
+// per edge, for both schedules.
 //
-// Covers shared potentials that are not Toeplitz bands (arbitrary CSC, as
-// produced by sparse_from_dense or the reference's random_sparse_potential,
-// synth.py:21-43) and, with m_max = M and idx[k][x] = k, the reference's
-// dense "standard" update (numba_kernels.py:35-41, 66-74).  One warp per
-// node; h is staged in shared memory so the gather h[idx] is a broadcast /
-// conflict-light LDS; entries of a column are visited in ascending x_i, the
-// reference's order, padded entries carry weight 0 (sum) / -inf (max).
+// Covers potentials that are not Toeplitz bands (arbitrary CSC, as produced
+// by sparse_from_dense or the reference's random_sparse_potential,
+// synth.py:21-43), per-edge (inhomogeneous) potentials -- which the reference
+// runs on its generic engine in the same grid pass order (bp.py:506-584,
+// 218-234) -- and, with m_max = M and idx[k][x] = k, the dense "standard"
+// update (numba_kernels.py:35-41, 66-74) for small M.  One warp per node
+// (synchronous) or per chain (sequential); h is staged in shared memory so
+// the gather h[idx] is a broadcast / conflict-light LDS; the entries of a
+// column are visited in ascending x_i, the reference order; padded entries
+// carry weight 0 (sum) / -inf (max).
+//
+// Potential storage: `idx` / `w` point at [n_pot][2 orientations][m_max][Ms];
+// with per-edge potentials pid_h[r*W + c] is the potential of edge
+// (n, n+1) and pid_v[r*W + c] that of (n, n+W) (global node ids).  Messages
+// from n to n+1 / n+W use orientation 0, to n-1 / n-W orientation 1 of the
+// edge's potential (bp.py:525, 443-463).
 #include "aux_kernels.cuh"
 #include "band_kernel.cuh"   // two_sum, shift_compensated, lanes_max
 
@@ -15,11 +25,56 @@ namespace sbp {
 constexpr int ELL_WARPS = 4;
 constexpr int ELL_QMAX = 8;   // Ms <= 256
 
-template <int DOM, int DIR>
-__device__ __forceinline__ void ell_emit(const EllArgs &a, const float (&h)[ELL_QMAX],
-                                         float *hs, int lane, bool active, long long node_l,
-                                         long long r, int c) {
-    constexpr int O = dir_orient(DIR);
+// Potential slot of the message node (r, c) -> direction dir.
+__device__ __forceinline__ long long ell_pot_slot(const EllArgs &a, long long r, int c, int dir) {
+    long long pid = 0;
+    if (a.pid_h) {
+        const long long n = r * a.W + c;
+        pid = dir == 0 ? a.pid_h[n] : dir == 1 ? a.pid_h[n - 1]
+            : dir == 2 ? a.pid_v[n] : a.pid_v[n - a.W];
+    }
+    return pid * 2 + dir_orient(dir);
+}
+
+// Exclusion vector h in the reference order (unary, slots 0..3 ascending,
+// skipping excl); max-sum error-free with the node shift, as the band kernel.
+template <int DOM>
+__device__ __forceinline__ void ell_h(const float (&g)[ELL_QMAX], const float (&m)[4][ELL_QMAX],
+                                      int excl, float (&h)[ELL_QMAX]) {
+    if (DOM == SBP_SUM) {
+#pragma unroll
+        for (int q = 0; q < ELL_QMAX; ++q) {
+            float v = g[q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k != excl) v *= m[k][q];
+            h[q] = v;
+        }
+    } else {
+        float s[ELL_QMAX], e[ELL_QMAX];
+#pragma unroll
+        for (int q = 0; q < ELL_QMAX; ++q) {
+            s[q] = g[q];
+            e[q] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k != excl) {
+                    float t, ee;
+                    two_sum(s[q], m[k][q], t, ee);
+                    s[q] = t;
+                    e[q] += ee;
+                }
+        }
+        shift_compensated<ELL_QMAX, 32>(s, e, h);
+    }
+}
+
+// The message of one directed edge: floor term + ELL correction (or the dense
+// sum when floor_term = 0 and the lists are full), then normalisation.
+template <int DOM>
+__device__ __forceinline__ bool ell_message(const EllArgs &a, const float (&h)[ELL_QMAX],
+                                            float *hs, int lane, long long pslot,
+                                            float (&out)[ELL_QMAX]) {
     const float NEG = -__builtin_huge_valf();
     float red = DOM == SBP_SUM ? 0.0f : NEG;
 #pragma unroll
@@ -35,17 +90,18 @@ __device__ __forceinline__ void ell_emit(const EllArgs &a, const float (&h)[ELL_
         red = DOM == SBP_SUM ? red + t : fmaxf(red, t);
     }
     __syncwarp();
+    const float fb = a.fbar_all ? a.fbar_all[pslot] : a.fbar[pslot & 1];
     const float base = !a.floor_term ? (DOM == SBP_SUM ? 0.0f : NEG)
-                                     : (DOM == SBP_SUM ? a.fbar[O] * red : a.fbar[O] + red);
-    float out[ELL_QMAX];
+                                     : (DOM == SBP_SUM ? fb * red : fb + red);
+    const long long off0 = pslot * a.pot_stride;
     float tot = DOM == SBP_SUM ? 0.0f : NEG;
 #pragma unroll
     for (int q = 0; q < ELL_QMAX; ++q) {
         const int x = lane + 32 * q;
         float acc = base;
         if (x < a.M) {
-            const int *ip = a.idx[O] + x;
-            const float *wp = a.w[O] + x;
+            const int *ip = a.idx + off0 + x;
+            const float *wp = a.w + off0 + x;
             for (int k = 0; k < a.m_max; ++k) {
                 const float hv = hs[ip[(long long)k * a.Ms]];
                 const float w = wp[(long long)k * a.Ms];
@@ -62,27 +118,24 @@ __device__ __forceinline__ void ell_emit(const EllArgs &a, const float (&h)[ELL_
         const float t = __shfl_xor_sync(SBP_FULL_MASK, tot, off);
         tot = DOM == SBP_SUM ? tot + t : fmaxf(tot, t);
     }
-    bool ok;
     if (DOM == SBP_SUM) {
-        ok = (tot > 0.0f) && !isinf(tot);
         const float inv = __frcp_rn(tot);
 #pragma unroll
         for (int q = 0; q < ELL_QMAX; ++q) out[q] *= inv;
-    } else {
-        ok = isfinite(tot);
-#pragma unroll
-        for (int q = 0; q < ELL_QMAX; ++q) out[q] -= tot;
+        return (tot > 0.0f) && !isinf(tot);
     }
-    if (!active) return;
-    const long long W = a.W;
-    const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
-    float *dst = a.msgs_out + dir_wslot(DIR) * a.slot_stride + (node_l + step) * a.Ms;
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) out[q] -= tot;
+    return isfinite(tot);
+}
+
+__device__ __forceinline__ void ell_store(const EllArgs &a, float *base, int lane,
+                                          const float (&out)[ELL_QMAX]) {
 #pragma unroll
     for (int q = 0; q < ELL_QMAX; ++q) {
         const int x = lane + 32 * q;
-        if (x < a.Ms) dst[x] = out[q];
+        if (x < a.Ms) base[x] = out[q];
     }
-    if (!ok && lane == 0) report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
 
 template <int DOM>
@@ -100,6 +153,7 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
     const float *gp = a.values + ((long long)(lr - 1) * a.W + c) * a.Ms;
     const float *mp = a.msgs_in + node_l * a.Ms;
     const float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
     float g[ELL_QMAX], m[4][ELL_QMAX];
 #pragma unroll
     for (int q = 0; q < ELL_QMAX; ++q) {
@@ -107,70 +161,81 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
         const bool in = x < a.Ms;
         g[q] = in ? gp[x] : PAD;
 #pragma unroll
-        if (!a.first) {
-            for (int k = 0; k < 4; ++k) m[k][q] = in ? mp[k * a.slot_stride + x] : PAD;
-        } else {
-            const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
-            for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
+            if (!a.first)
+                m[k][q] = in ? mp[k * a.slot_stride + x] : PAD;
+            else
                 m[k][q] = x >= a.M ? PAD
                                    : (DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f);
         }
     }
-    float h[ELL_QMAX];
-    const bool has_r = c + 1 < a.W, has_l = c > 0, has_d = r + 1 < a.H, has_u = r > 0;
-    if (DOM == SBP_SUM) {
-#define SBP_H(E0, E1, E2)                                                                  \
-    for (int q = 0; q < ELL_QMAX; ++q) h[q] = ((g[q] * m[E0][q]) * m[E1][q]) * m[E2][q];
-        if (has_u) { SBP_H(1, 2, 3) ell_emit<DOM, 3>(a, h, hs, lane, true, node_l, r, c); }
-        if (has_l) { SBP_H(0, 2, 3) ell_emit<DOM, 1>(a, h, hs, lane, true, node_l, r, c); }
-        if (has_r) { SBP_H(0, 1, 3) ell_emit<DOM, 0>(a, h, hs, lane, true, node_l, r, c); }
-        if (has_d) { SBP_H(0, 1, 2) ell_emit<DOM, 2>(a, h, hs, lane, true, node_l, r, c); }
-#undef SBP_H
-    } else {
-        // Same error-free (TwoSum) sums and shift as the band kernel, in the
-        // same operation order, so fast (band) and standard (dense) max-sum
-        // stay bit-identical as in the reference (bp.py:325-333).
-        float sa[ELL_QMAX], ea[ELL_QMAX], s2[ELL_QMAX], e2[ELL_QMAX];
-        for (int q = 0; q < ELL_QMAX; ++q) two_sum(g[q], m[0][q], sa[q], ea[q]);
-        if (has_u) {
-            for (int q = 0; q < ELL_QMAX; ++q) {
-                float t, e;
-                two_sum(g[q], m[1][q], s2[q], e2[q]);
-                two_sum(s2[q], m[2][q], t, e); s2[q] = t; e2[q] += e;
-                two_sum(s2[q], m[3][q], t, e); s2[q] = t; e2[q] += e;
-            }
-            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
-            ell_emit<DOM, 3>(a, h, hs, lane, true, node_l, r, c);
-        }
-        if (has_l) {
-            for (int q = 0; q < ELL_QMAX; ++q) {
-                float t, e;
-                two_sum(sa[q], m[2][q], s2[q], e); e2[q] = ea[q] + e;
-                two_sum(s2[q], m[3][q], t, e); s2[q] = t; e2[q] += e;
-            }
-            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
-            ell_emit<DOM, 1>(a, h, hs, lane, true, node_l, r, c);
-        }
+    const bool has[4] = {c + 1 < a.W, c > 0, r + 1 < a.H, r > 0};
+    const long long W = a.W;
+#pragma unroll
+    for (int dir = 0; dir < 4; ++dir) {
+        if (!has[dir]) continue;
+        float h[ELL_QMAX], out[ELL_QMAX];
+        ell_h<DOM>(g, m, dir_excl(dir), h);
+        const bool ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), out);
+        const long long step = dir == 0 ? 1 : dir == 1 ? -1 : dir == 2 ? W : -W;
+        ell_store(a, a.msgs_out + dir_wslot(dir) * a.slot_stride + (node_l + step) * a.Ms, lane,
+                  out);
+        if (!ok && lane == 0)
+            report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, dir));
+    }
+}
+
+// Sequential (canonical) pass over chains, one warp per chain; see
+// chain_kernel.cuh for the pass geometry and the failure key.
+template <int DOM>
+__global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_constant__ EllArgs a) {
+    __shared__ float hs_all[ELL_WARPS][32 * ELL_QMAX];
+    const int lane = threadIdx.x & 31;
+    float *hs = hs_all[threadIdx.x >> 5];
+    const int dir = a.pass;
+    const long long H = a.H, W = a.W;
+    const long long n_lines = dir <= 1 ? H : W, len = dir <= 1 ? W - 1 : H - 1;
+    const long long stride = dir <= 1 ? W : 1;
+    const long long step = dir == 0 ? 1 : dir == 1 ? -1 : dir == 2 ? W : -W;
+    const long long origin = dir == 1 ? W - 1 : dir == 3 ? (H - 1) * W : 0;
+    const int wslot = dir_wslot(dir), excl = dir_excl(dir);
+    const long long line = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (line >= n_lines) return;   // warp-uniform
+    const float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    float *msgs = a.msgs_out;
+    const long long S = a.slot_stride;
+    long long src = line * stride + origin;
+    float chain[ELL_QMAX];
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) {
+        const int x = lane + 32 * q;
+        chain[q] = x < a.Ms ? msgs[wslot * S + (src + W) * a.Ms + x] : PAD;
+    }
+    for (long long pos = 0; pos < len; ++pos, src += step) {
+        float g[ELL_QMAX], m[4][ELL_QMAX];
+#pragma unroll
         for (int q = 0; q < ELL_QMAX; ++q) {
-            float t, e;
-            two_sum(sa[q], m[1][q], t, e); sa[q] = t; ea[q] += e;
+            const int x = lane + 32 * q;
+            const bool in = x < a.Ms;
+            g[q] = in ? a.values[src * a.Ms + x] : PAD;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                m[k][q] = k == wslot ? chain[q]
+                        : (k == excl || !in) ? PAD : msgs[k * S + (src + W) * a.Ms + x];
         }
-        if (has_r) {
-            for (int q = 0; q < ELL_QMAX; ++q) {
-                float e;
-                two_sum(sa[q], m[3][q], s2[q], e); e2[q] = ea[q] + e;
-            }
-            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
-            ell_emit<DOM, 0>(a, h, hs, lane, true, node_l, r, c);
+        float h[ELL_QMAX];
+        ell_h<DOM>(g, m, excl, h);
+        const long long r = src / W;
+        const int c = (int)(src % W);
+        const bool ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), chain);
+        ell_store(a, msgs + wslot * S + (src + step + W) * a.Ms, lane, chain);
+        if (!ok && lane == 0) {
+            const unsigned long long key = ((unsigned long long)a.iteration << 40) |
+                                           ((unsigned long long)dir << 38) |
+                                           (unsigned long long)(line * len + pos);
+            atomicMin(a.err, key);
         }
-        if (has_d) {
-            for (int q = 0; q < ELL_QMAX; ++q) {
-                float e;
-                two_sum(sa[q], m[2][q], s2[q], e); e2[q] = ea[q] + e;
-            }
-            shift_compensated<ELL_QMAX, 32>(s2, e2, h);
-            ell_emit<DOM, 2>(a, h, hs, lane, true, node_l, r, c);
-        }
+        __syncwarp();
     }
 }
 
@@ -183,6 +248,24 @@ cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s) {
     else
         ell_iter_kernel<SBP_MAX><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_ell_sweep(int domain, const EllArgs &a, cudaStream_t s) {
+    for (int dir = 0; dir < 4; ++dir) {
+        EllArgs b = a;
+        b.pass = dir;
+        const long long lines = dir <= 1 ? a.H : a.W;
+        const long long len = dir <= 1 ? a.W - 1 : a.H - 1;
+        if (len <= 0) continue;
+        const long long blocks = (lines + ELL_WARPS - 1) / ELL_WARPS;
+        if (domain == SBP_SUM)
+            ell_chain_kernel<SBP_SUM><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
+        else
+            ell_chain_kernel<SBP_MAX><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace sbp

@@ -34,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .plan import PotentialPlan, plan_potential
+from .plan import PotentialPlan, plan_per_edge, plan_potential
 
 __all__ = ["SYNCHRONOUS", "SEQUENTIAL", "DegenerateMessageError", "DegenerateBeliefError",
            "UnsafePotentialError", "SweepStats", "BeliefTable", "MessageStore", "GridEngine",
@@ -95,6 +95,8 @@ class BeliefTable:
 # ---------------------------------------------------------------------------
 
 def _shared_potential(model):
+    """The potential shared by every edge, or None when edges carry their own
+    (the reference then runs its generic engine, bp.py:652-654)."""
     pot = getattr(model, "shared_potential", None)
     if pot is not None:
         return pot
@@ -103,10 +105,19 @@ def _shared_potential(model):
         return None
     first = pots[0]
     if any(p is not first for p in pots):
-        raise NotImplementedError(
-            "GPU grid engine needs one potential shared by all edges (reference grid-engine "
-            "precondition, bp.py:652-654); per-edge potentials are not supported")
+        return None
     return first
+
+
+def _unique_potentials(model) -> list:
+    """Reference bp.py:436-440 (identity-deduplicated, first-seen order)."""
+    pot = getattr(model, "shared_potential", None)
+    if pot is not None:
+        return [pot]
+    seen: dict = {}
+    for p in model.potentials:
+        seen.setdefault(id(p), p)
+    return list(seen.values())
 
 
 def _validate(model, kernel: str, domain: str, pot) -> None:
@@ -180,8 +191,9 @@ class GridEngine:
         self.domain = domain
         self.kernel = kernel
         self.device = torch.device(device) if device is not None else torch.device("cuda")
-        pot = _shared_potential(model)
-        _validate(model, kernel, domain, pot)
+        pot = _shared_potential(model) if model.n_edges else None
+        for p in (_unique_potentials(model) if model.n_edges else []):
+            _validate(model, kernel, domain, p)
         self.schedule = schedule
         if schedule == SEQUENTIAL and (r0 != 0 or (rows is not None and rows != self.H)):
             raise NotImplementedError("sequential sweeps run on the whole grid (no strips)")
@@ -195,10 +207,9 @@ class GridEngine:
         self.plan: PotentialPlan | None = None
         if pot is not None:
             self.plan = plan_potential(pot, domain, kernel, self.M, self.Ms)
-            if schedule == SEQUENTIAL and self.plan.kind != L.SBP_POT_BAND:
-                raise NotImplementedError(
-                    "the GPU sequential schedule supports banded (Toeplitz) potentials with the "
-                    f"fast/pruned kernels; got a {self.plan.kind_name} plan (kernel={kernel!r})")
+        elif model.n_edges:
+            self.plan = plan_per_edge(model, domain, kernel, self.M, self.Ms)
+        if self.plan is not None:
             self._pot_struct = self._make_pot_struct(self.plan)
         with torch.cuda.device(self.device):
             shape = (4, self.rows + 2, self.W, self.Ms)
@@ -226,9 +237,18 @@ class GridEngine:
             idx = torch.from_numpy(np.ascontiguousarray(plan.ell_idx)).to(self.device)
             w = torch.from_numpy(np.ascontiguousarray(plan.ell_w, dtype=np.float32)).to(self.device)
             plan.device_arrays = [idx, w]
-            for o in range(2):
-                s.ell_idx[o] = idx[o].data_ptr()
-                s.ell_w[o] = w[o].data_ptr()
+            # orientation 1 directly follows orientation 0 ([.., 2, m_max, Ms])
+            step = plan.m_max * self.Ms * 4
+            s.ell_idx[0], s.ell_idx[1] = idx.data_ptr(), idx.data_ptr() + step
+            s.ell_w[0], s.ell_w[1] = w.data_ptr(), w.data_ptr() + step
+            if plan.n_pot:
+                fb = torch.from_numpy(np.ascontiguousarray(plan.fbar_all, dtype=np.float32)).to(
+                    self.device)
+                ph = torch.from_numpy(plan.pid_h).to(self.device)
+                pv = torch.from_numpy(plan.pid_v).to(self.device)
+                plan.device_arrays += [fb, ph, pv]
+                s.n_pot = plan.n_pot
+                s.fbar_all, s.pid_h, s.pid_v = fb.data_ptr(), ph.data_ptr(), pv.data_ptr()
             if plan.dense_t is not None:
                 t = torch.from_numpy(np.ascontiguousarray(plan.dense_t, dtype=np.float32)).to(
                     self.device)
@@ -538,8 +558,8 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
     mode = _schedule_mode(schedule)
     if n_sweeps < 0:
         raise ValueError(f"n_sweeps must be >= 0, got {n_sweeps}")
-    pot = _shared_potential(model) if model.n_edges else None
-    _validate(model, kernel, domain, pot)
+    for p in (_unique_potentials(model) if model.n_edges else []):
+        _validate(model, kernel, domain, p)
     stats = SweepStats()
     if model.n_edges == 0 or n_sweeps == 0:
         store = MessageStore(model, domain, engine=None)
@@ -563,7 +583,10 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
                 break
     torch.cuda.synchronize(eng.device)
     stats.sweep_seconds = [a.elapsed_time(b) / 1e3 for a, b in events]
-    stats.madds = eng.plan.madds_per_update * stats.n_updates
+    if eng.plan.madds_per_sweep is not None:
+        stats.madds = eng.plan.madds_per_sweep * stats.sweeps_run
+    else:
+        stats.madds = eng.plan.madds_per_update * stats.n_updates
     eng.raise_if_degenerate()
     store = MessageStore(model, domain, engine=eng)
     store.stats = stats

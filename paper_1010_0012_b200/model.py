@@ -243,12 +243,14 @@ class _SharedPotentials(Sequence):
 
 
 class GridMrf:
-    """4-connected H x W grid MRF with one shared pairwise potential.
+    """4-connected H x W grid MRF with one shared pairwise potential, or one
+    potential per edge (a sequence in the reference edge order).
 
     Attribute surface matches the reference ``MrfModel`` for grid models
     (``M``, ``unaries``, ``log_unaries``, ``edges``, ``potentials``,
     ``grid_shape``, ``n_nodes``, ``n_edges``).  ``shared_potential`` lets the
-    engine skip the identity scan over ``potentials``.
+    engine skip the identity scan over ``potentials``; it is None for
+    per-edge potentials.
     """
 
     def __init__(self, height: int, width: int, M: int, unaries, potential,
@@ -267,7 +269,16 @@ class GridMrf:
         if not (u > 0).any(axis=1).all():
             bad = int(np.flatnonzero(~(u > 0).any(axis=1))[0])
             raise ValueError(f"unary table of node {bad} has no positive entry")
-        if potential.M != M:
+        per_edge = None
+        if isinstance(potential, (list, tuple)):
+            per_edge = list(potential)
+            n_edges = height * (width - 1) + width * (height - 1)
+            if len(per_edge) != n_edges:
+                raise ValueError(f"need one potential per edge ({n_edges}), got {len(per_edge)}")
+            for p in per_edge:
+                if p.M != M:
+                    raise ValueError(f"potential label count {p.M} != model label count {M}")
+        elif potential.M != M:
             raise ValueError(f"potential label count {potential.M} != model label count {M}")
         if log_unaries is not None:
             log_unaries = np.ascontiguousarray(log_unaries, dtype=np.float64)
@@ -278,7 +289,8 @@ class GridMrf:
         self.grid_shape = (int(height), int(width))
         self.unaries = _frozen(u)
         self._log_unaries = log_unaries
-        self.shared_potential = potential
+        self.shared_potential = None if per_edge is not None else potential
+        self._per_edge = per_edge
         self._edges = None
 
     @property
@@ -298,6 +310,8 @@ class GridMrf:
 
     @property
     def potentials(self) -> Sequence:
+        if self._per_edge is not None:
+            return self._per_edge
         return _SharedPotentials(self.shared_potential, self.n_edges)
 
     @property

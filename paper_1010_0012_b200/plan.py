@@ -45,6 +45,12 @@ class PotentialPlan:
     ell_w: np.ndarray | None = None         # (2, m_max, Ms) f64
     dense_t: np.ndarray | None = None       # (2, Ms, Ms) f64, f(x_i=k, x_j=x) at [o, k, x]
     madds_per_update: int = 0
+    # per-edge potentials (n_pot > 0): ell_idx / ell_w are (n_pot, 2, m_max, Ms)
+    n_pot: int = 0
+    fbar_all: np.ndarray | None = None      # (n_pot, 2)
+    pid_h: np.ndarray | None = None         # (H*W,) int32, potential of edge (n, n+1)
+    pid_v: np.ndarray | None = None         # (H*W,) int32, potential of edge (n, n+W)
+    madds_per_sweep: int | None = None      # per-edge: the reference counter summed over edges
     device_arrays: list = field(default_factory=list)
 
     @property
@@ -110,6 +116,79 @@ def _ell(sp_list, Ms: int, pad: float):
         idx[o, k, cols] = np.asarray(sp.col_indices)
         w[o, k, cols] = np.asarray(wts)
     return m_max, idx, w
+
+
+def _oriented_lists(pot, domain: str, kernel: str, M: int):
+    """[(indptr, indices, weights, fbar)] for orientations 0 and 1 (bp.py:443-463)."""
+    pad = 0.0 if domain == "sum" else -np.inf
+    use = pot.to_log() if domain == "max" else pot
+    if kernel == "standard":
+        table = _dense_table(use)
+        out = []
+        for t in (table, table.T):           # f_o(x_i = k, x_j = x) at [k][x]
+            indptr = np.arange(M + 1, dtype=np.int64) * M
+            indices = np.tile(np.arange(M, dtype=np.int64), M)
+            out.append((indptr, indices, np.ascontiguousarray(t.T).ravel(), 0.0))
+        return out, pad
+    if not _is_sparse(use):
+        raise TypeError(f"kernel={kernel!r} requires SparseTruncatedPotential, "
+                        f"got {type(pot).__name__}")
+    out = []
+    for sp in (use, use.transpose()):
+        if kernel == "fast":
+            w = sp.col_residuals if domain == "sum" else sp.col_values
+        else:
+            w = sp.col_values
+        out.append((np.asarray(sp.col_indptr), np.asarray(sp.col_indices), np.asarray(w),
+                    float(sp.fbar)))
+    return out, pad
+
+
+def plan_per_edge(model, domain: str, kernel: str, M: int, Ms: int) -> PotentialPlan:
+    """Per-edge (inhomogeneous) potentials -- the reference's generic engine
+    (bp.py:506-584): unique potentials (by object identity, in edge order),
+    both orientations each, ELL arrays stacked, one potential id per edge."""
+    H, W = model.grid_shape
+    uid: dict = {}
+    unique = []
+    pid_h = np.full(H * W, -1, dtype=np.int32)
+    pid_v = np.full(H * W, -1, dtype=np.int32)
+    edges = np.asarray(model.edges)
+    pots = list(model.potentials)
+    for (a, b), pot in zip(edges, pots):
+        k = uid.setdefault(id(pot), len(unique))
+        if k == len(unique):
+            unique.append(pot)
+        if b - a == 1 and W > 1:
+            pid_h[a] = k
+        else:
+            pid_v[a] = k
+    lists = []
+    pad = 0.0
+    for pot in unique:
+        ol, pad = _oriented_lists(pot, domain, kernel, M)
+        lists.append(ol)
+    m_max = max(1, max(int(np.diff(l[0]).max(initial=0)) for ol in lists for l in ol))
+    U = len(unique)
+    idx = np.zeros((U, 2, m_max, Ms), dtype=np.int32)
+    w = np.full((U, 2, m_max, Ms), pad, dtype=np.float64)
+    fb = np.zeros((U, 2), dtype=np.float64)
+    for u, ol in enumerate(lists):
+        for o, (indptr, indices, wts, fbar) in enumerate(ol):
+            lens = np.diff(indptr)
+            cols = np.repeat(np.arange(len(lens)), lens)
+            kk = np.arange(indptr[-1]) - indptr[cols]
+            idx[u, o, kk, cols] = indices
+            w[u, o, kk, cols] = wts
+            fb[u, o] = fbar
+    per_sweep = 0
+    for pot in pots:
+        per_sweep += 2 * (M * M if kernel == "standard" else madds_per_update(pot, kernel, M))
+    kind = L.SBP_POT_DENSE if kernel == "standard" else L.SBP_POT_ELL
+    return PotentialPlan(kind, L.SBP_SUM if domain == "sum" else L.SBP_MAX, kernel,
+                         0 if kernel != "fast" else 1, M, Ms, (0.0, 0.0), m_max=m_max,
+                         ell_idx=idx, ell_w=w, n_pot=U, fbar_all=fb, pid_h=pid_h, pid_v=pid_v,
+                         madds_per_update=0, madds_per_sweep=per_sweep)
 
 
 def plan_potential(pot, domain: str, kernel: str, M: int, Ms: int,

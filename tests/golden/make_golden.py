@@ -132,6 +132,85 @@ def sync_iter(domain, kernel, H, W, M, vals, mi, mo,
 KID = {"standard": 0, "fast": 1, "pruned": 2}
 
 
+@njit
+def generic_sync_iter(domain, kernel, M, src, rev, opid, in_indptr, in_eids, vals, old, new,
+                      tablesT, fbars, indptrs, indices_flat, values_flat, residuals_flat, fails):
+    """One synchronous iteration over every directed edge, composed from the
+    reference generic engine's own bodies (numba_kernels.py:422-485)."""
+    h = np.empty(M, dtype=np.float64)
+    out = np.empty(M, dtype=np.float64)
+    nf = 0
+    for d in range(src.shape[0]):
+        q = opid[d]
+        nk._generic_h(vals, old, in_indptr, in_eids, src[d], rev[d], h, M, domain == 1)
+        if domain == 0:
+            if kernel == 0:
+                nk._std_sum(h, tablesT[q], out, M)
+            elif kernel == 1:
+                nk._fast_sum(h, fbars[q], indptrs[q], indices_flat, residuals_flat, out, M)
+            else:
+                nk._pruned_sum(h, indptrs[q], indices_flat, values_flat, out, M)
+            ok = nk._normalize_sum_into(out, new[d], M)
+        else:
+            if kernel == 0:
+                nk._std_max(h, tablesT[q], out, M)
+            elif kernel == 1:
+                nk._fast_max(h, fbars[q], indptrs[q], indices_flat, values_flat, out, M)
+            else:
+                nk._pruned_max(h, indptrs[q], indices_flat, values_flat, out, M)
+            ok = nk._normalize_max_into(out, new[d], M)
+        if not ok and nf < fails.shape[0]:
+            fails[nf] = d
+            nf += 1
+    return nf
+
+
+def ref_generic_sync_run(model, iters, domain, kernel):
+    eng = sparsebp.bp._GenericEngine(model, kernel, domain)
+    a = sparsebp.MessageStore(model, domain).data.copy()
+    b = a.copy()
+    fails = np.zeros(64, dtype=np.int64)
+    for _ in range(iters):
+        nf = generic_sync_iter(0 if domain == "sum" else 1, KID[kernel], model.M, eng.src,
+                               eng.rev, eng.opid, eng.in_indptr, eng.in_eids, eng.values_in, a,
+                               b, eng.tablesT, eng.fbars, eng.indptrs, eng.indices_flat,
+                               eng.values_flat, eng.residuals_flat, fails)
+        assert nf == 0
+        a, b = b, a
+    return a
+
+
+def save_per_edge(name, model, results):
+    pots = model.potentials
+    M = model.M
+    arrays = {"unaries": np.asarray(model.unaries), "log_unaries": np.asarray(model.log_unaries),
+              "grid_shape": np.array(model.grid_shape),
+              "pe_fbar": np.array([p.fbar for p in pots]),
+              "pe_indptr": np.stack([p.col_indptr for p in pots]),
+              "pe_indices": np.concatenate([p.col_indices for p in pots]),
+              "pe_values": np.concatenate([p.col_values for p in pots])}
+    arrays.update(results)
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+
+
+def add_per_edge_cases(tag, model, sweeps):
+    for dom in ("sum", "max"):
+        for ker in ("fast", "standard"):
+            data = ref_generic_sync_run(model, sweeps, dom, ker)
+            name = f"pe_sync_{tag}_{dom}_{ker}"
+            save_per_edge(name, model, {"store": data})
+            manifest["cases"][name] = {"kind": "pe_sync", "domain": dom, "kernel": ker,
+                                       "iters": sweeps, "store_sha": sha(data),
+                                       "grid": list(model.grid_shape), "M": model.M}
+            store = sparsebp.run_sweeps(model, sweeps, kernel=ker, domain=dom)
+            name = f"pe_seq_{tag}_{dom}_{ker}"
+            save_per_edge(name, model, {"store": store.data})
+            manifest["cases"][name] = {"kind": "pe_seq", "domain": dom, "kernel": ker,
+                                       "sweeps": sweeps, "store_sha": sha(store.data),
+                                       "madds": int(store.stats.madds),
+                                       "grid": list(model.grid_shape), "M": model.M}
+
+
 def oriented_args(model, domain, kernel):
     """Mirror of bp._grid_setup (bp.py:466-489) as flat argument tuples."""
     pot = model.potentials[0].to_log() if domain == "max" else model.potentials[0]
@@ -393,6 +472,12 @@ def main():
         save_full(name, chain, {"marginals": ex.marginals, "map_config": ex.map_config})
         manifest["cases"][name] = {"kind": "exact", "grid": [1, W], "M": M,
                                    "map_unique": bool(ex.map_unique), "log_Z": ex.log_Z}
+
+    # --- per-edge (inhomogeneous) potentials: the reference generic engine -----
+    for k in range(3):
+        rng = np.random.default_rng(200 + k)
+        pm = ref_synth.random_grid_model(rng, max_side=7, max_M=20, shared_potential=False)
+        add_per_edge_cases(f"r{k}", pm, 4)
 
     # --- BASELINE C1 / C2 (digests + labels) --------------------------------
     c1, _, _ = ref_stereo_model(48, 64, 16, 1.0, 2.0, 5.0, 0)

@@ -31,6 +31,16 @@ def load_case(name: str):
     z = dict(np.load(GOLDEN / f"{name}.npz"))
     H, W = (int(v) for v in z["grid_shape"])
     M = z["unaries"].shape[1]
+    if "pe_indptr" in z:           # one potential per edge (reference generic engine)
+        pots, off = [], 0
+        for e, indptr in enumerate(z["pe_indptr"]):
+            n = int(indptr[-1])
+            pots.append(SparseTruncatedPotential(M, float(z["pe_fbar"][e]), indptr,
+                                                 z["pe_indices"][off:off + n],
+                                                 z["pe_values"][off:off + n]))
+            off += n
+        model = GridMrf(H, W, M, z["unaries"], pots, log_unaries=z["log_unaries"])
+        return model, z
     if "col_indptr" in z:
         pot = SparseTruncatedPotential(M, float(z["fbar"]), z["col_indptr"], z["col_indices"],
                                        z["col_values"])

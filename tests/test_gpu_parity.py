@@ -312,3 +312,16 @@ def test_staged_and_register_kernels_agree_bitwise(tmp_path, name, domain):
     b = _run_subprocess({"SBP_STAGED": "0", "SBP_BAND_VL": "8"}, name, domain, 7,
                         tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
+
+
+
+@pytest.mark.parametrize("name", sorted(n for n, e in MAN["cases"].items() if e["kind"] == "pe_sync"))
+def test_per_edge_potentials_synchronous(name):
+    e = MAN["cases"][name]
+    model, z = load_case(name)
+    store = sbp.run_sweeps(model, e["iters"], kernel=e["kernel"], domain=e["domain"],
+                           schedule=SYNC)
+    if e["domain"] == "sum":
+        assert oracle.rel_deviation(store.data, z["store"], floor=1e-30) <= SUM_TOL
+    else:
+        assert max_dev(store.data, z["store"]) <= MAX_TOL

@@ -95,3 +95,26 @@ def test_sequential_convergence_tol():
         prev = msgs
     assert ref.stats.converged
     assert abs(ref.stats.sweeps_run - n) <= 1
+
+
+
+@pytest.mark.parametrize("name", sorted(n for n, e in MAN["cases"].items() if e["kind"] == "pe_seq"))
+def test_per_edge_potentials_sequential(name):
+    """The reference default schedule with per-edge potentials (its generic
+    engine) -- the GPU runs it with the warp-per-chain ELL kernel."""
+    e = MAN["cases"][name]
+    model, z = load_case(name)
+    store = sbp.run_sweeps(model, e["sweeps"], kernel=e["kernel"], domain=e["domain"])
+    assert store.stats.madds == e["madds"]
+    if e["domain"] == "sum":
+        assert oracle.rel_deviation(store.data, z["store"], floor=1e-30) <= TOL
+    else:
+        assert max_dev(store.data, z["store"]) <= TOL
+
+
+def test_general_shared_potential_sequential():
+    """A shared non-band (ELL) potential in the default schedule."""
+    name = "sync_random0_sum"
+    model, _ = load_case(name)
+    for domain in ("sum", "max"):
+        check_seq(model, 4, domain)

@@ -175,3 +175,18 @@ def test_unary_field_matches_reference(name, dims):
     e = MAN["unaries"][name]
     assert sha_raw(right) == e["right"]
     assert sha(u) == e["unaries"] and sha(lu) == e["log_unaries"]
+
+
+@pytest.mark.parametrize("name", sorted(n for n, e in CASES.items()
+                                        if e["kind"] in ("pe_sync", "pe_seq")))
+def test_per_edge_potentials_bitwise(name):
+    """Per-edge potentials: the reference generic engine (bp.py:506-584),
+    synchronous composition and its own sequential run_sweeps."""
+    e = CASES[name]
+    model, z = load_case(name)
+    if e["kind"] == "pe_sync":
+        msgs4 = oracle.sync_run(model, e["iters"], e["domain"], e["kernel"], nthreads=2)
+    else:
+        msgs4, madds = oracle.seq_run(model, e["sweeps"], e["domain"], e["kernel"])
+        assert madds == e["madds"]
+    assert sha(oracle.store_data(model, msgs4)) == e["store_sha"]
