@@ -136,15 +136,17 @@ class StripRunner:
 
 
 def run_rank(strip, iters: int, rank: int, world: int, group=None, overlap: bool = True,
-             compute_stream=None, interior_stream=None) -> None:
+             compute_stream=None, interior_stream=None, dist=None) -> None:
     """Per-rank loop of the distributed strip decomposition.
 
     ``strip`` is this rank's strip (rank k owns strip k, top to bottom).
     With CUDA tensors the exchange is NCCL send/recv; with CPU tensors it is
     gloo.  When ``overlap`` is set and streams are given, the interior rows run
-    on ``interior_stream`` while the halos travel.
+    on ``interior_stream`` while the halos travel.  ``dist`` defaults to
+    ``torch.distributed`` (tests substitute an in-process transport).
     """
-    import torch.distributed as dist
+    if dist is None:
+        import torch.distributed as dist
 
     boundary, interior = _split_rows(strip.rows)
     cuda = strip.next_buffer().is_cuda
