@@ -40,6 +40,20 @@ struct BandArgs {
     float w[2][2 * SBP_MAX_R + 1];
 };
 
+// Per-iteration view of the buffers: which buffer is read / written, the
+// first row of the range, the iteration index (error key) and whether the
+// incoming messages are the initial ones.  The plain kernels build it from
+// BandArgs; the wavefront kernel changes it per work item.
+struct IterCtx {
+    const float *msgs_in;
+    float *msgs_out;
+    int lr_begin, iteration, first;
+};
+
+__device__ __forceinline__ IterCtx iter_of(const BandArgs &a) {
+    return IterCtx{a.msgs_in, a.msgs_out, a.lr_begin, a.iteration, a.first};
+}
+
 template <int N>
 struct Vec8Loader {
     static __device__ __forceinline__ void load(float (&dst)[N], const float *src) {
@@ -225,22 +239,24 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
 }
 
 template <int DOM, int VL, int LP, int R, int O>
-__device__ __forceinline__ void emit_direction(const BandArgs &a, const float (&h)[VL], int DIR,
-                                               int j, int x0, bool active, long long node_l,
-                                               long long r, int c) {
+__device__ __forceinline__ void emit_direction(const BandArgs &a, const IterCtx &it,
+                                               const float (&h)[VL], int DIR, int j, int x0,
+                                               bool active, long long node_l, long long r,
+                                               int c) {
     float out[VL];
     const bool ok = band_message<DOM, VL, LP, R, O>(a, h, j, x0, out);
     if (!active) return;
     const long long W = a.W;
     const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
-    float *dst = a.msgs_out + dir_wslot(DIR) * a.slot_stride + (node_l + step) * a.Ms + x0;
+    float *dst = it.msgs_out + dir_wslot(DIR) * a.slot_stride + (node_l + step) * a.Ms + x0;
     Vec8Loader<VL>::store(dst, out);
-    if (!ok && j == 0) report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, DIR));
+    if (!ok && j == 0) report_failure(a.err, it.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
 
 // The four messages of one node from its unary and incoming vectors.
 template <int DOM, int VL, int LP, int R>
-__device__ __forceinline__ void band_group_body(const BandArgs &a, const float (&g)[VL],
+__device__ __forceinline__ void band_group_body(const BandArgs &a, const IterCtx &it,
+                                                const float (&g)[VL],
                                                 const float (&m0)[VL], const float (&m1)[VL],
                                                 const float (&m2)[VL], const float (&m3)[VL],
                                                 int j, int x0, bool valid, long long node_l,
@@ -256,24 +272,24 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const float (
         if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ((g[i] * m1[i]) * m2[i]) * m3[i];
-            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, h, 3, j, x0, valid && has_u, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, it, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = (ab[i] * m2[i]) * m3[i];
-            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, h, 1, j, x0, valid && has_l, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, it, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
 #pragma unroll
         for (int i = 0; i < VL; ++i) ab[i] = ab[i] * m1[i];                 // g m0 m1
         if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ab[i] * m3[i];
-            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, h, 0, j, x0, valid && has_r, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, it, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
 #pragma unroll
             for (int i = 0; i < VL; ++i) h[i] = ab[i] * m2[i];
-            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, h, 2, j, x0, valid && has_d, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, it, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     } else {
         // Max-sum: h = ln g + sum of three messages.  Its entries can reach
@@ -294,7 +310,7 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const float (
                 two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, h, 3, j, x0, valid && has_u, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, it, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
 #pragma unroll
@@ -304,7 +320,7 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const float (
                 two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, h, 1, j, x0, valid && has_l, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, it, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
 #pragma unroll
         for (int i = 0; i < VL; ++i) {                                       // g + m0 + m1
@@ -318,7 +334,7 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const float (
                 two_sum(sa[i], m3[i], s2[i], e); e2[i] = ea[i] + e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, h, 0, j, x0, valid && has_r, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, it, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
 #pragma unroll
@@ -327,21 +343,22 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const float (
                 two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
             }
             shift_compensated<VL, LP>(s2, e2, h);
-            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, h, 2, j, x0, valid && has_d, node_l, r, c);
+            emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, it, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     }
 }
 
 // One warp-group of PPW = 32/LP nodes (flattened pixel group `grp`).
 template <int DOM, int VL, int LP, int R>
-__device__ __forceinline__ void band_group(const BandArgs &a, long long grp, long long npix) {
+__device__ __forceinline__ void band_group(const BandArgs &a, const IterCtx &it, long long grp,
+                                   long long npix) {
     constexpr int PPW = 32 / LP;
     const int lane = threadIdx.x & 31;
     const int j = lane % LP;
     long long p = grp * PPW + lane / LP;
     const bool valid = p < npix;
     if (!valid) p = npix - 1;
-    const int lr = a.lr_begin + (int)(p / a.W);
+    const int lr = it.lr_begin + (int)(p / a.W);
     const int c = (int)(p % a.W);
     const long long r = (long long)a.r0 + lr - 1;
     const long long node_l = (long long)lr * a.W + c;
@@ -349,8 +366,8 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
 
     float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
     Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
-    const float *mi = a.msgs_in + node_l * a.Ms + x0;
-    if (!a.first) {
+    const float *mi = it.msgs_in + node_l * a.Ms + x0;
+    if (!it.first) {
         Vec8Loader<VL>::load(m0, mi);
         Vec8Loader<VL>::load(m1, mi + a.slot_stride);
         Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
@@ -369,7 +386,7 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
         }
     }
 
-    band_group_body<DOM, VL, LP, R>(a, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
+    band_group_body<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
 }
 
 // Rolled variant for potentials whose two orientations carry the same band
@@ -378,15 +395,15 @@ __device__ __forceinline__ void band_group(const BandArgs &a, long long grp, lon
 // the instruction footprint 4x -- the unrolled kernel spills the I-cache for
 // wide bands (ncu: 34 % of issue slots lost to instruction fetch at R = 32).
 template <int DOM, int VL, int LP, int R>
-__device__ __forceinline__ void band_group_rolled(const BandArgs &a, long long grp,
-                                                  long long npix) {
+__device__ __forceinline__ void band_group_rolled(const BandArgs &a, const IterCtx &it, long long grp,
+                                   long long npix) {
     constexpr int PPW = 32 / LP;
     const int lane = threadIdx.x & 31;
     const int j = lane % LP;
     long long p = grp * PPW + lane / LP;
     const bool valid = p < npix;
     if (!valid) p = npix - 1;
-    const int lr = a.lr_begin + (int)(p / a.W);
+    const int lr = it.lr_begin + (int)(p / a.W);
     const int c = (int)(p % a.W);
     const long long r = (long long)a.r0 + lr - 1;
     const long long node_l = (long long)lr * a.W + c;
@@ -394,8 +411,8 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, long long g
 
     float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
     Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
-    const float *mi = a.msgs_in + node_l * a.Ms + x0;
-    if (!a.first) {
+    const float *mi = it.msgs_in + node_l * a.Ms + x0;
+    if (!it.first) {
         Vec8Loader<VL>::load(m0, mi);
         Vec8Loader<VL>::load(m1, mi + a.slot_stride);
         Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
@@ -462,7 +479,7 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, long long g
             }
             shift_compensated<VL, LP>(s2, e2, h);
         }
-        emit_direction<DOM, VL, LP, R, 0>(a, h, dir, j, x0, valid && hd, node_l, r, c);
+        emit_direction<DOM, VL, LP, R, 0>(a, it, h, dir, j, x0, valid && hd, node_l, r, c);
     }
 }
 
@@ -511,6 +528,7 @@ template <int DOM, int VL, int LP, int R>
 __global__ void __launch_bounds__(32 * STG_WARPS)
 band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
+    const IterCtx it = iter_of(a);
     constexpr int VEC = 32 * VL;                 // floats of one vector for one group
     extern __shared__ __align__(128) float stg_smem[];
     __shared__ __align__(8) unsigned long long bars[STG_WARPS][2];
@@ -588,7 +606,7 @@ band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
             }
         }
         __syncwarp();   // every lane has read stage st before it is refilled
-        band_group_body<DOM, VL, LP, R>(a, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
+        band_group_body<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
         st ^= 1;
     }
 }
@@ -643,6 +661,7 @@ template <int DOM, int VL, int LP, int R, bool ROLLED>
 __global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : 3))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
+    const IterCtx it = iter_of(a);
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long ngroups = (npix + PPW - 1) / PPW;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -650,8 +669,8 @@ band_iter_kernel(const __grid_constant__ BandArgs a) {
     if (a.prefetch && grp < ngroups) prefetch_group(a, grp, npix, PPW);
     for (; grp < ngroups; grp += nwarps) {
         if (a.prefetch && grp + nwarps < ngroups) prefetch_group(a, grp + nwarps, npix, PPW);
-        if constexpr (ROLLED) band_group_rolled<DOM, VL, LP, R>(a, grp, npix);
-        else band_group<DOM, VL, LP, R>(a, grp, npix);
+        if constexpr (ROLLED) band_group_rolled<DOM, VL, LP, R>(a, it, grp, npix);
+        else band_group<DOM, VL, LP, R>(a, it, grp, npix);
     }
 }
 
