@@ -325,3 +325,57 @@ def test_per_edge_potentials_synchronous(name):
         assert oracle.rel_deviation(store.data, z["store"], floor=1e-30) <= SUM_TOL
     else:
         assert max_dev(store.data, z["store"]) <= MAX_TOL
+
+
+@pytest.mark.parametrize("M,T", [(1, 1.0), (2, 1.5), (3, 2.0), (7, 2.0), (13, 3.0), (24, 4.0),
+                                 (100, 5.0), (129, 3.0), (200, 9.0)])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_label_counts_and_padding(M, T, domain):
+    """Odd and non-power-of-two M (padded label stride), M=1, band radius close
+    to M: the padding must stay an exact no-op."""
+    H, W = 7, max(M, 9) if M <= 16 else 11
+    left, right, _ = synth.noisy_stereo_pair(H, max(W, M), M, 5.0, M)
+    u, lu = synth.stereo_unary_field(left, right, M, 0.1, 255.0)
+    model = sbp.GridMrf(H, max(W, M), M, u, sbp.truncated_linear_potential(M, 0.6, T),
+                        log_unaries=lu)
+    check_run(model, 6, domain)
+
+
+@pytest.mark.parametrize("H,W", [(1, 2), (2, 1), (1, 40), (40, 1), (3, 3)])
+def test_degenerate_shapes(H, W):
+    u = np.random.default_rng(H * 100 + W).uniform(0.05, 1.0, size=(H * W, 16))
+    model = sbp.GridMrf(H, W, 16, u, sbp.truncated_linear_potential(16, 1.0, 3.0))
+    for domain in ("sum", "max"):
+        check_run(model, 5, domain)
+
+
+@pytest.mark.slow
+def test_large_grid_64bit_offsets():
+    """A grid whose message buffers exceed 2^31 floats (int64 offsets):
+    4100 x 4100 nodes, M=32 -> 2.15e9 floats per buffer."""
+    H = W = 4100
+    M = 32
+    rng = np.random.default_rng(0)
+    cfg = synth.CONFIGS["C2"]
+    values = rng.uniform(0.1, 1.0, size=(H * W, M))
+    from paper_1010_0012_b200.engine import GridEngine
+    model = synth.StripModel(cfg)
+    model.grid_shape = (H, W)
+    model.n_edges = H * (W - 1) + W * (H - 1)
+    eng = GridEngine(model, "sum", "fast", values=values)
+    eng.step(3)
+    torch.cuda.synchronize()
+    eng.raise_if_degenerate()
+    # the last node's messages are normalised and finite
+    last = eng.current[:, H, W - 1, :M]
+    assert torch.isfinite(last).all()
+    assert abs(float(last[0].sum()) - 1.0) < 1e-5 and abs(float(last[1].sum()) - 1.0) < 1e-5
+    # and the bottom-right 12x12 corner matches the oracle on the corner crop
+    # (after 3 iterations a message depends on the 3-neighbourhood only)
+    r0, c0 = H - 12, W - 12
+    idx = (np.arange(r0, H)[:, None] * W + np.arange(c0, W)[None, :]).ravel()
+    crop = sbp.GridMrf(12, 12, M, values[idx], model.shared_potential)
+    ref = oracle.sync_run(crop, 3, "sum", "fast")
+    got = eng.current[:, H - 5 + 1, W - 5:W, :M].double().cpu().numpy()   # rows H-5.., local +1
+    want = ref[:, (12 - 5) * 12 + 7: (12 - 5) * 12 + 12]
+    assert oracle.rel_deviation(got, want, floor=1e-30) <= SUM_TOL
