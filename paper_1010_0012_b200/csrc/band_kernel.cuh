@@ -34,7 +34,6 @@ struct BandArgs {
     long long slot_stride;  // (rows+2)*W*Ms
     int H, W, M, Ms, r0, lr_begin, lr_end, iteration, floor_term;
     int first;   // iteration 0: incoming messages are the reference init, not read
-    int prefetch;  // L2-prefetch the next pixel group (persistent loop)
     int pass;      // sequential mode: pass direction 0..3 (chain_kernel.cuh)
     float fbar[2];
     float w[2][2 * SBP_MAX_R + 1];
@@ -636,27 +635,10 @@ cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// L2 prefetch of one pixel group's five input vectors (unary + 4 incoming
-// slots).  node_l and the value index are linear in the flattened pixel
-// index, so each vector of a group is one contiguous chunk.
-__device__ __forceinline__ void prefetch_group(const BandArgs &a, long long grp, long long npix,
-                                               int ppw) {
-    const int lane = threadIdx.x & 31;
-    if (lane > 4 || (lane < 4 && a.first)) return;
-    const long long p0 = grp * ppw;
-    if (p0 >= npix) return;
-    const long long n = (npix - p0 < ppw ? npix - p0 : ppw);
-    const unsigned bytes = (unsigned)(n * a.Ms * 4);
-    const float *src = lane == 4
-        ? a.values + ((long long)(a.lr_begin - 1) * a.W + p0) * a.Ms
-        : a.msgs_in + lane * a.slot_stride + ((long long)a.lr_begin * a.W + p0) * a.Ms;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-
 // Persistent grid-stride kernel: each warp walks pixel groups grp, grp + T,
-// ... (T = resident warps) and prefetches its next group into L2 before
-// computing the current one, keeping HBM requests in flight during the
-// band arithmetic.
+// ... (T = resident warps).  (An L2 prefetch of the next group measured
+// slower on C4 and was dropped; the TMA-staged variant below is the
+// latency-hiding version.)
 template <int DOM, int VL, int LP, int R, bool ROLLED>
 __global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : 3))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
@@ -666,9 +648,7 @@ band_iter_kernel(const __grid_constant__ BandArgs a) {
     const long long ngroups = (npix + PPW - 1) / PPW;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (a.prefetch && grp < ngroups) prefetch_group(a, grp, npix, PPW);
     for (; grp < ngroups; grp += nwarps) {
-        if (a.prefetch && grp + nwarps < ngroups) prefetch_group(a, grp + nwarps, npix, PPW);
         if constexpr (ROLLED) band_group_rolled<DOM, VL, LP, R>(a, it, grp, npix);
         else band_group<DOM, VL, LP, R>(a, it, grp, npix);
     }

@@ -51,15 +51,6 @@ int check_grid(const sbp_grid *g) {
 
 const int kRadii[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32};
 
-int band_prefetch() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBP_PREFETCH");
-        v = e ? atoi(e) != 0 : 0;   // measured slower on C4 (tools/sweep_r01.sh)
-    }
-    return v;
-}
-
 // Band kernel variant choice, from the B200 A/B runs (tools/ab_vl.sh,
 // tools/ab_staged.sh; profiles/r01_kernel_variants.md).  Environment
 // overrides: SBP_BAND_VL=8|16, SBP_STAGED=0|1, SBP_ROLL_MIN_R=<r>.
@@ -219,7 +210,6 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.floor_term = pot->floor_term;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
-        a.prefetch = band_prefetch();
         const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
         for (int o = 0; o < 2; ++o) {
             a.fbar[o] = pot->fbar[o];
