@@ -319,14 +319,17 @@ def run_ours(args, cfg):
     achieved = (B / world) / (kern_ms / 1e3) / 1e9
     launches_per_step = args.iters * (1 if world == 1 else 3) + 1   # iterations + labels
 
-    # e2e through the public API with host buffers (rank 0 at N=1 only)
+    # e2e through the public API with host buffers; CPU baseline at N=1 only
     e2e = None
     cpu = None
-    if world == 1 and not args.kernel_only:
-        e2e = e2e_public_api(args, cfg, torch)
-        ups, cores, sample = cpu_sample(cfg, args.domain)
-        cpu = {"value": ups, "unit": "updates/s", "cores": cores, "kind": "port",
-               "sample": sample}
+    if not args.kernel_only:
+        if world == 1:
+            e2e = e2e_public_api(args, cfg, torch)
+            ups, cores, sample = cpu_sample(cfg, args.domain)
+            cpu = {"value": ups, "unit": "updates/s", "cores": cores, "kind": "port",
+                   "sample": sample}
+        else:
+            e2e = e2e_strips(args, cfg, torch, rank, world, dev)
     if rank != 0:
         return
     line = {
@@ -418,6 +421,47 @@ def e2e_public_api(args, cfg, torch):
                               "d2h_bytes_per_step": int(labels_u.size * 4),
                               "ms_per_step": dt_u * 1e3,
                               "api": "run_sweeps(GridMrf with pinned f64 unaries) + map_labels"}}
+
+
+def e2e_strips(args, cfg, torch, rank, world, dev):
+    """N>1 end to end: every rank uploads its rows of the pinned image pair,
+    builds its unaries on its GPU, runs the strip iterations (NCCL halos) and
+    the labels are gathered to rank 0's host.  Wall time, max over ranks."""
+    import torch.distributed as dist
+
+    import paper_1010_0012_b200 as sbp
+    from paper_1010_0012_b200 import synth
+    from paper_1010_0012_b200.distributed import gather_labels, run_sweeps_strips
+    left, right, _ = synth.noisy_stereo_pair(cfg.height, cfg.width, cfg.M, cfg.sigma, 0)
+    imgs = []
+    for img in (left, right):
+        t = torch.empty(img.shape, dtype=torch.uint8, pin_memory=True)
+        t.numpy()[...] = img
+        imgs.append(t.numpy())
+    params = sbp.StereoParams(M=cfg.M, alpha=cfg.alpha, T_b=cfg.T, beta=cfg.beta, T_u=cfg.T_u)
+
+    def once():
+        model = sbp.build_stereo_mrf(imgs[0], imgs[1], params)
+        eng = run_sweeps_strips(model, args.iters, domain=args.domain, device=dev)
+        return gather_labels(eng)
+
+    once()
+    reps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        labels = once()
+    torch.cuda.synchronize()
+    dt = torch.tensor([(time.perf_counter() - t0) / reps], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dt = float(dt.item())
+    rows = cfg.height // world + 1
+    return {"value": cfg.n_directed * args.iters / dt, "unit": "updates/s",
+            "h2d_bytes_per_step": int(2 * rows * cfg.width),
+            "d2h_bytes_per_step": int(cfg.height * cfg.width * 4) if rank == 0 else 0,
+            "ms_per_step": dt * 1e3, "n_labels": None if labels is None else int(labels.size),
+            "api": "build_stereo_mrf + distributed.run_sweeps_strips + gather_labels"}
 
 
 def main():

@@ -92,3 +92,13 @@ def test_threaded_ranks_match_whole_grid(world, domain):
     assert not errors, errors
     got = np.concatenate(parts, axis=1).reshape(4, H * W, model.M)
     np.testing.assert_array_equal(got, full)
+
+
+def test_run_sweeps_strips_single_rank():
+    """The multi-GPU public entry point at world size 1 equals run_sweeps."""
+    from paper_1010_0012_b200.distributed import gather_labels, run_sweeps_strips
+    left, right, _ = synth.noisy_stereo_pair(30, 50, 16, 5.0, 4)
+    model = sbp.build_stereo_mrf(left, right, sbp.StereoParams(M=16, T_b=2, beta=0.1, T_u=255))
+    eng = run_sweeps_strips(model, 9)
+    want = sbp.map_labels(sbp.run_sweeps(model, 9, schedule="synchronous"))
+    np.testing.assert_array_equal(gather_labels(eng), want)
