@@ -379,3 +379,39 @@ def test_large_grid_64bit_offsets():
     got = eng.current[:, H - 5 + 1, W - 5:W, :M].double().cpu().numpy()   # rows H-5.., local +1
     want = ref[:, (12 - 5) * 12 + 7: (12 - 5) * 12 + 12]
     assert oracle.rel_deviation(got, want, floor=1e-30) <= SUM_TOL
+
+
+class RefLikeModel:
+    """Attribute surface of the reference ``sparsebp.MrfModel`` (mrf.py:288-398):
+    plain ``potentials`` list (one object repeated), ``edges`` array, lazy
+    ``log_unaries`` -- no ``shared_potential`` shortcut."""
+
+    def __init__(self, model):
+        self.M = model.M
+        self.unaries = np.asarray(model.unaries)
+        self._lu = np.asarray(model.log_unaries)
+        self.edges = np.asarray(model.edges)
+        self.potentials = [model.shared_potential] * len(self.edges)
+        self.grid_shape = model.grid_shape
+
+    @property
+    def log_unaries(self):
+        return self._lu
+
+    @property
+    def n_nodes(self):
+        return self.unaries.shape[0]
+
+    @property
+    def n_edges(self):
+        return len(self.edges)
+
+
+@pytest.mark.parametrize("schedule", [None, "synchronous"])
+def test_reference_shaped_model_object(schedule):
+    base = synth.build_config_model(synth.CONFIGS["C2"], height=18, width=30)
+    ref_like = RefLikeModel(base)
+    for domain in ("sum", "max"):
+        a = sbp.run_sweeps(ref_like, 6, domain=domain, schedule=schedule).data
+        b = sbp.run_sweeps(base, 6, domain=domain, schedule=schedule).data
+        np.testing.assert_array_equal(a, b)

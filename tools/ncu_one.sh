@@ -4,7 +4,7 @@
 # CSV and drops the (large) .ncu-rep so gpurun_out stays small.
 tag=$1; shift
 "$@" > gpurun_out/plain_$tag.log 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on -k regex:band_iter -s 3 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:${NCU_KERNEL:-band_iter} -s ${NCU_SKIP:-3} -c 1 \
     -o /tmp/prof_$tag "$@" > gpurun_out/ncu_$tag.log 2>&1 || exit 2
 ncu -i /tmp/prof_$tag.ncu-rep --page raw --csv > gpurun_out/raw_$tag.csv 2>/dev/null
 ncu -i /tmp/prof_$tag.ncu-rep --page source --csv > gpurun_out/src_$tag.csv 2>/dev/null
