@@ -65,4 +65,8 @@ for schedule in ("synchronous", "sequential"):
         row["label_mismatch_decided"] = int(((lab != ref_lab) & decided).sum())
         row["label_mismatch_all"] = int((lab != ref_lab).sum())
         row["near_ties_excluded"] = int((~decided).sum())
+        mism = lab != ref_lab
+        # f64 top-2 gap at the nodes whose labels differ: ~1e-15 means an
+        # exact tie of the real-valued scores (sums of multiples of 0.1)
+        row["max_gap_at_mismatch"] = float(oracle.top2_gap(ref_scores)[mism].max()) if mism.any() else 0.0
         print(json.dumps(row), flush=True)
