@@ -118,3 +118,17 @@ def test_general_shared_potential_sequential():
     model, _ = load_case(name)
     for domain in ("sum", "max"):
         check_seq(model, 4, domain)
+
+
+@pytest.mark.parametrize("kernel,sweeps", [("standard", 3), ("pruned", 1)])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_sequential_other_kernels(kernel, sweeps, domain):
+    """Dense ("standard", warp-per-chain ELL kernel) and pruned (band chain
+    kernel without the floor term) in the reference default schedule."""
+    model = synth.build_config_model(synth.CONFIGS["C1"], height=12, width=20)
+    ref = oracle.store_data(model, oracle.seq_run(model, sweeps, domain, kernel)[0])
+    store = sbp.run_sweeps(model, sweeps, kernel=kernel, domain=domain)
+    if domain == "sum":
+        assert oracle.rel_deviation(store.data, ref, floor=1e-30) <= TOL
+    else:
+        assert max_dev(store.data, ref) <= TOL
