@@ -34,6 +34,23 @@ int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+// libsbp links its own (static) CUDA runtime, whose per-thread current device
+// is independent of the one torch sets.  Every launching entry point
+// therefore selects the device that owns its buffers first; otherwise rank k
+// of a multi-GPU run would launch on device 0 with device k's pointers.
+int select_device_of(const void *p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged) return -1;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != attr.device) cudaSetDevice(attr.device);
+    return attr.device;
+}
+
 int cuda_status(cudaError_t e, const char *where) {
     if (e == cudaSuccess) return SBP_OK;
     return fail(SBP_ECUDA, "%s: %s", where, cudaGetErrorString(e));
@@ -154,6 +171,7 @@ int sbp_padded_labels(int M) {
 int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!msgs) return fail(SBP_EINVAL, "msgs is NULL");
+    select_device_of(msgs);
     return cuda_status(sbp::launch_init_msgs(msgs, g->H, g->W, g->M, g->Ms, g->r0, g->rows,
                                              domain, ghosts_only ? 1 : 0, (cudaStream_t)stream),
                        "sbp_init_msgs");
@@ -162,6 +180,7 @@ int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs, v
 int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!src || !dst) return fail(SBP_EINVAL, "NULL pointer");
+    select_device_of(dst);
     return cuda_status(sbp::launch_load_values(src, dst, (long long)g->rows * g->W, g->M, g->Ms,
                                                domain, (cudaStream_t)stream),
                        "sbp_load_values");
@@ -172,6 +191,7 @@ int sbp_stereo_values(const sbp_grid *g, int domain, const uint8_t *left, const 
     if (int rc = check_grid(g)) return rc;
     if (!left || !right || !dst) return fail(SBP_EINVAL, "NULL pointer");
     if (!(beta > 0) || !(T_u > 0)) return fail(SBP_EINVAL, "beta and T_u must be > 0");
+    select_device_of(dst);
     return cuda_status(sbp::launch_stereo_values(left, right, (long long)g->rows, g->W, g->M,
                                                  g->Ms, beta, T_u, domain, dst,
                                                  (cudaStream_t)stream),
@@ -188,6 +208,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         return fail(SBP_EINVAL, "bad row range [%d, %d) of %d rows", lr_begin, lr_end, g->rows);
     if (lr_begin == lr_end) return SBP_OK;
     if (iteration < 0 || iteration >= (1 << 23)) return fail(SBP_EINVAL, "bad iteration index");
+    select_device_of(msgs_out);
     const long long slot = (long long)(g->rows + 2) * g->W * g->Ms;
     cudaStream_t s = (cudaStream_t)stream;
     if (pot->kind == SBP_POT_BAND) {
@@ -253,6 +274,7 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
     if (!pot || !values || !msgs || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "sequential sweeps need the full grid");
     if (sweep < 0 || sweep >= (1 << 23)) return fail(SBP_EINVAL, "bad sweep index");
+    select_device_of(msgs);
     if (pot->kind != SBP_POT_BAND) {
         sbp::EllArgs a;
         if (int rc = ell_args(g, pot, &a)) return rc;
@@ -328,6 +350,7 @@ int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float 
                 unsigned long long *bad_node, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!values || !msgs) return fail(SBP_EINVAL, "NULL pointer");
+    select_device_of(msgs);
     return cuda_status(sbp::launch_beliefs(domain, values, msgs, g->W, g->M, g->Ms, g->rows,
                                            beliefs, normalizers, labels, bad_node,
                                            (cudaStream_t)stream),
@@ -338,6 +361,7 @@ int sbp_gather_store(const sbp_grid *g, const float *msgs, float *out, void *str
     if (int rc = check_grid(g)) return rc;
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "gather needs the full grid");
     if (!msgs || !out) return fail(SBP_EINVAL, "NULL pointer");
+    select_device_of(msgs);
     return cuda_status(sbp::launch_gather_store(msgs, g->H, g->W, g->M, g->Ms, out,
                                                 (cudaStream_t)stream),
                        "sbp_gather_store");
@@ -347,6 +371,7 @@ int sbp_max_abs_diff(const sbp_grid *g, const float *a, const float *b, float *o
                      void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!a || !b || !out) return fail(SBP_EINVAL, "NULL pointer");
+    select_device_of(a);
     return cuda_status(sbp::launch_max_abs_diff(a, b, g->W, g->M, g->Ms, g->rows, out,
                                                 (cudaStream_t)stream),
                        "sbp_max_abs_diff");
