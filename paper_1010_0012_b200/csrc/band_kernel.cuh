@@ -523,7 +523,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
     }
 }
 
-template <int DOM, int VL, int LP, int R>
+// NS = 2: double buffer, the next group's copy is issued before waiting for
+// the current one.  NS = 1: one buffer, the next copy is issued as soon as the
+// current group has moved to registers (half the shared memory, for VL = 16).
+template <int DOM, int VL, int LP, int R, int NS>
 __global__ void __launch_bounds__(32 * STG_WARPS)
 band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
@@ -534,7 +537,7 @@ band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = lane % LP, q = lane / LP;
     const int x0 = j * VL;
-    float *buf = stg_smem + warp * (2 * 5 * VEC);
+    float *buf = stg_smem + warp * (NS * 5 * VEC);
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long ngroups = (npix + PPW - 1) / PPW;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -567,7 +570,7 @@ band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     int st = 0;
     if (grp < ngroups) issue(grp, 0);
     for (; grp < ngroups; grp += nwarps) {
-        if (grp + nwarps < ngroups) issue(grp + nwarps, st ^ 1);
+        if (NS == 2 && grp + nwarps < ngroups) issue(grp + nwarps, st ^ 1);
         mbar_wait(&bars[warp][st], (phase >> st) & 1);
         phase ^= 1u << st;
         long long p = grp * PPW + q;
@@ -605,24 +608,25 @@ band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
             }
         }
         __syncwarp();   // every lane has read stage st before it is refilled
+        if (NS == 1 && grp + nwarps < ngroups) issue(grp + nwarps, 0);
         band_group_body<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
-        st ^= 1;
+        if (NS == 2) st ^= 1;
     }
 }
 
-template <int DOM, int VL, int LP, int R>
+template <int DOM, int VL, int LP, int R, int NS>
 cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
     constexpr int PPW = 32 / LP;
-    const size_t smem = (size_t)STG_WARPS * 2 * 5 * 32 * VL * sizeof(float);
+    const size_t smem = (size_t)STG_WARPS * NS * 5 * 32 * VL * sizeof(float);
     static int resident = 0, sms = 0;
     if (!resident) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(band_iter_staged_kernel<DOM, VL, LP, R>,
+        cudaFuncSetAttribute(band_iter_staged_kernel<DOM, VL, LP, R, NS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &resident, band_iter_staged_kernel<DOM, VL, LP, R>, 32 * STG_WARPS, smem);
+            &resident, band_iter_staged_kernel<DOM, VL, LP, R, NS>, 32 * STG_WARPS, smem);
         if (resident < 1) resident = 1;
     }
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
@@ -631,7 +635,7 @@ cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
-    band_iter_staged_kernel<DOM, VL, LP, R><<<(unsigned)blocks, 32 * STG_WARPS, smem, s>>>(a);
+    band_iter_staged_kernel<DOM, VL, LP, R, NS><<<(unsigned)blocks, 32 * STG_WARPS, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -708,7 +712,7 @@ BandLaunchFn pick_band_r(int R) {
 
 // VL = 16 is compiled only where the sweeps chose it (sum, Ms >= 128); the
 // max domain always runs VL = 8 (its TwoSum state spills at VL = 16).
-template <int MS, int DOM, int VL>
+template <int MS, int DOM, int VL, int NS>
 BandLaunchFn pick_band_staged_r(int R) {
     if constexpr (VL > MS) {
         return nullptr;
@@ -717,7 +721,7 @@ BandLaunchFn pick_band_staged_r(int R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
         if constexpr (RR < MS && RR <= 16)                                \
-            return &launch_band_staged<DOM, VL, MS / VL, RR>;             \
+            return &launch_band_staged<DOM, VL, MS / VL, RR, NS>;         \
         else return nullptr;
             SBP_BAND_RADII(SBP_CASE)
 #undef SBP_CASE
@@ -729,7 +733,12 @@ BandLaunchFn pick_band_staged_r(int R) {
 // rolled: 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged unrolled (R <= 16)
 template <int MS, int DOM>
 BandLaunchFn pick_band_dom(int vl, int R, int rolled) {
-    if (rolled == 2) return vl == 8 ? pick_band_staged_r<MS, DOM, 8>(R) : nullptr;
+    if (rolled == 2) {
+        if (vl == 8) return pick_band_staged_r<MS, DOM, 8, 2>(R);
+        if constexpr (DOM == SBP_SUM && MS >= 128)
+            if (vl == 16) return pick_band_staged_r<MS, DOM, 16, 1>(R);
+        return nullptr;
+    }
     if (vl == 8) return rolled ? pick_band_r<MS, DOM, 8, true>(R) : pick_band_r<MS, DOM, 8, false>(R);
     if constexpr (DOM == SBP_SUM && MS >= 128) {
         if (vl == 16)

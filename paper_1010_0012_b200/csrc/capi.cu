@@ -95,12 +95,16 @@ BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
         // staged VL=8: +7 % on C3 max, +2.5 % on C5 T=9 sum, ~= VL=16 on C4 sum;
         // plain VL=16 wins for the lightest band (C5 T=2: R=1 at Ms=256)
         const bool staged_default = domain == SBP_MAX || Ms <= 128 || Rk >= 4;
-        const int staged = env_int("SBP_STAGED", staged_default ? 1 : 0) && Rk <= 16;
+        // SBP_STAGED: 0 register-loaded, 1 staged VL=8 (2 buffers), 2 staged VL=16
+        // (1 buffer; sum, Ms >= 128)
+        int staged = env_int("SBP_STAGED", staged_default ? 1 : 0);
+        if (Rk > 16) staged = 0;
+        if (staged == 2 && !(domain == SBP_SUM && Ms >= 128)) staged = 1;
         c.variant = staged ? 2 : 0;
-        c.vl = staged ? 8 : ((domain == SBP_SUM && Ms >= 128) ? 16 : 8);
+        c.vl = staged == 1 ? 8 : (staged == 2 ? 16 : ((domain == SBP_SUM && Ms >= 128) ? 16 : 8));
     }
     const int v = env_int("SBP_BAND_VL", 0);
-    if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128 && c.variant != 2)) c.vl = v;
+    if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = v;
     return c;
 }
 
