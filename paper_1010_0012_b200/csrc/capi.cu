@@ -92,9 +92,10 @@ BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
         c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
         c.variant = 1;
     } else {
-        // staged VL=8: +7 % on C3 max, +2.5 % on C5 T=9 sum, ~= VL=16 on C4 sum;
-        // plain VL=16 wins for the lightest band (C5 T=2: R=1 at Ms=256)
-        const bool staged_default = domain == SBP_MAX || Ms <= 128 || Rk >= 4;
+        // staged VL=8: +7 % on C3 max-sum and +2.5 % on C5 T=9 sum; the plain
+        // VL=16 kernel is best for Ms = 128 sum (C4: 2.30 vs 2.34-2.37 ms cold,
+        // 2.57 vs 2.57-2.65 ms sustained) and for the lightest band (C5 T=2)
+        const bool staged_default = domain == SBP_MAX || Ms < 128 || (Ms >= 256 && Rk >= 4);
         // SBP_STAGED: 0 register-loaded, 1 staged VL=8 (2 buffers), 2 staged VL=16
         // (1 buffer; sum, Ms >= 128)
         int staged = env_int("SBP_STAGED", staged_default ? 1 : 0);
