@@ -644,7 +644,7 @@ cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
 // slower on C4 and was dropped; the TMA-staged variant below is the
 // latency-hiding version.)
 template <int DOM, int VL, int LP, int R, bool ROLLED>
-__global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : 3))
+__global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : (R <= 8 ? 4 : 3)))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
     const IterCtx it = iter_of(a);
