@@ -700,7 +700,7 @@ BandLaunchFn pick_band_r(int R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
         if constexpr (RR < MS && (!ROLLED || RR >= 24) &&                   \
-                      (VL == 8 || ROLLED || RR <= 3))                         \
+                      (VL == 8 || ROLLED || RR <= 8))                         \
             return &launch_band<DOM, VL, MS / VL, RR, ROLLED>;             \
         else return nullptr;
             SBP_BAND_RADII(SBP_CASE)

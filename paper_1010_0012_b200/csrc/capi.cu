@@ -92,21 +92,45 @@ BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
         c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
         c.variant = 1;
     } else {
-        // staged VL=8: +7 % on C3 max-sum and +2.5 % on C5 T=9 sum; the plain
-        // VL=16 kernel is best for Ms = 128 sum (C4: 2.30 vs 2.34-2.37 ms cold,
-        // 2.57 vs 2.57-2.65 ms sustained) and for the lightest band (C5 T=2)
-        const bool staged_default = domain == SBP_MAX || Ms < 128 || (Ms >= 256 && Rk >= 4);
+        // Defaults from the B200 A/B (profiles/r01_ab_sustained_3.txt,
+        // r01_ab_staged_3.txt; kernel ms per iteration):
+        //   max-sum, any Ms         staged VL=8   (C3 0.355 vs 0.372)
+        //   sum, Ms=128, R <= 8     plain VL=16   (C4 2.21 cold / 2.43 sustained
+        //                                          vs 2.30 / 2.56 plain VL=8)
+        //   sum, Ms=256, R <= 4     staged VL=16  (C5 T=5 1.50 vs 1.56)
+        //   sum, Ms=256, R 5..8     plain VL=16   (C5 T=9 1.54 vs 1.65)
+        //   sum, Ms >= 128, R > 8   staged VL=8   (C5 T=17 2.35 vs 2.44)
+        //   sum, Ms < 128           plain VL=8    (C2: variants within noise)
+        const bool wide = domain == SBP_SUM && Ms >= 128;
+        int staged_default = 0;
+        if (domain == SBP_MAX || (wide && Rk > 8)) staged_default = 1;
+        else if (wide && Ms >= 256 && Rk <= 4) staged_default = 2;
         // SBP_STAGED: 0 register-loaded, 1 staged VL=8 (2 buffers), 2 staged VL=16
         // (1 buffer; sum, Ms >= 128)
-        int staged = env_int("SBP_STAGED", staged_default ? 1 : 0);
+        int staged = env_int("SBP_STAGED", staged_default);
         if (Rk > 16) staged = 0;
         if (staged == 2 && !(domain == SBP_SUM && Ms >= 128)) staged = 1;
         c.variant = staged ? 2 : 0;
-        c.vl = staged == 1 ? 8 : (staged == 2 ? 16 : ((domain == SBP_SUM && Ms >= 128) ? 16 : 8));
+        c.vl = staged == 1 ? 8 : (staged == 2 ? 16
+                                  : ((wide && Rk <= 8) ? 16 : 8));
     }
     const int v = env_int("SBP_BAND_VL", 0);
     if (v == 8 || (v == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = v;
     return c;
+}
+
+sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled);
+
+// The launch function actually used: the chosen variant if compiled, else
+// the always-compiled register-loaded VL=8 kernel (ch is updated to match).
+sbp::BandLaunchFn band_resolve(int Ms, int dom, int Rk, BandChoice &ch) {
+    sbp::BandLaunchFn fn = band_fn(Ms, dom, ch.vl, Rk, ch.variant);
+    if (!fn) {
+        ch.vl = 8;
+        ch.variant = 0;
+        fn = band_fn(Ms, dom, 8, Rk, 0);
+    }
+    return fn;
 }
 
 bool band_symmetric(const sbp_potential *pot) {
@@ -221,9 +245,8 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         int Rk = 0;
         for (int r : kRadii)
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
-        const BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
-        sbp::BandLaunchFn fn = Rk ? band_fn(g->Ms, pot->domain, ch.vl, Rk, ch.variant) : nullptr;
-        if (!fn && Rk) fn = band_fn(g->Ms, pot->domain, 8, Rk, 0);   // always compiled
+        BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
+        sbp::BandLaunchFn fn = Rk ? band_resolve(g->Ms, pot->domain, Rk, ch) : nullptr;
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
         sbp::BandArgs a;
@@ -337,7 +360,8 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         if (sequential) {
             snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
         } else {
-            const BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
+            BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
+            if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);
             snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
                      ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom, ch.vl,
                      g->Ms / ch.vl, Rk, ch.variant == 1 ? ",rolled" : "");

@@ -205,3 +205,42 @@ def test_oracle_sync_matches_per_edge_composition():
                 for x in range(M):
                     s += res[x]
                 np.testing.assert_array_equal(out[ws, dst], res * (1.0 / s))
+
+
+def _plan_name(cfg_name, domain, sequential=False):
+    cfg = synth.CONFIGS[cfg_name]
+    Ms = L.lib().sbp_padded_labels(cfg.M)
+    pl = plan.plan_potential(cfg.build_potential(), domain, "fast", cfg.M, Ms)
+
+    class _E:   # the fields _make_pot_struct reads for a band plan
+        dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
+    s = engine.GridEngine._make_pot_struct(_E(), pl)
+    g = L.SbpGrid(cfg.height, cfg.width, cfg.M, Ms, 0, cfg.height)
+    buf = ctypes.create_string_buffer(128)
+    L.check(L.lib().sbp_plan_name(ctypes.byref(g), ctypes.byref(s), 1 if sequential else 0,
+                                  buf, 128))
+    return buf.value.decode()
+
+
+@pytest.mark.parametrize("name,domain,expect", [
+    ("C4", "sum", "band_iter_kernel<sum,VL=16,LP=8,R=7>"),
+    ("C3", "max", "band_iter_staged_kernel<max,VL=8,LP=8,R=3>"),
+    ("C2", "sum", "band_iter_kernel<sum,VL=8,LP=4,R=2>"),
+    ("C5_T5", "sum", "band_iter_staged_kernel<sum,VL=16,LP=16,R=4>"),
+    ("C5_T9", "sum", "band_iter_kernel<sum,VL=16,LP=16,R=8>"),
+    ("C5_T17", "sum", "band_iter_staged_kernel<sum,VL=8,LP=32,R=16>"),
+])
+def test_default_kernel_choice(name, domain, expect):
+    # host-only: names the instantiation sbp_iterate would launch
+    assert _plan_name(name, domain) == expect
+
+
+def test_plan_name_reports_the_fallback(monkeypatch):
+    # plain VL=16 is not compiled for R=16: the launch falls back to VL=8 and
+    # the reported name must say so (it did not, once)
+    monkeypatch.setenv("SBP_STAGED", "0")
+    monkeypatch.setenv("SBP_BAND_VL", "16")
+    assert _plan_name("C5_T17", "sum") == "band_iter_kernel<sum,VL=8,LP=32,R=16>"
+    assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=16,LP=8,R=7>"
+    monkeypatch.setenv("SBP_BAND_VL", "8")
+    assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=8,LP=16,R=7>"

@@ -31,7 +31,7 @@ B = 4 * M * (H * W + 2 * cfg.n_directed)
 pot = model.shared_potential
 F = cfg.n_directed * 2 * (pot.nnz + 2 * M) if kernel != "standard" else cfg.n_directed * 2 * M * M
 peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
-print(json.dumps({"config": name, "domain": domain, "kernel": kernel, "plan": eng.plan.kind_name,
+print(json.dumps({"config": name, "domain": domain, "kernel": kernel, "kernel_name": eng.kernel_name, "plan": eng.plan.kind_name,
                   "R": eng.plan.R, "median_ms": steady, "min_ms": min(ms),
                   "GBps": B / steady / 1e6, "hbm_frac": B / steady / 1e6 / peak,
                   "TFLOPs": F / steady / 1e9, "updates_per_s": cfg.n_directed / steady * 1e3}))
