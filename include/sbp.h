@@ -17,6 +17,9 @@
  *                         one SYNCHRONOUS iteration of all directed updates
  *                         of a row range: _grid_h_* (:194-227) -> _fast_* /
  *                         _std_* / _pruned_* (:35-101) -> _norm_*_store (:248-271)
+ *   sbp_iterate_fused  <- bp.py:660-676 (the run_sweeps loop): 1..4 consecutive
+ *                         synchronous iterations in one launch (sbp_iterate's
+ *                         arithmetic, intermediate messages kept in L2)
  *   sbp_sweep          <- bp.py:492-503 + numba_kernels.py:274-407: one canonical
  *                         sequential sweep (the reference default schedule)
  *   sbp_beliefs        <- bp.py:711-744      `compute_beliefs`,
@@ -128,6 +131,22 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
                         const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
                         int iteration, int flags, unsigned long long *err, void *stream);
 
+/* `levels` (1..4) consecutive synchronous iterations over the whole strip in
+ * ONE persistent cooperative launch (temporal blocking: a row wavefront with
+ * `lag` rows between levels; the intermediate messages stay in L2 and are
+ * discarded there once read).  Level l reads buffer l % 2 of (msgs_a, msgs_b)
+ * and writes the other: the result is in msgs_a for even `levels`, msgs_b
+ * for odd; the intermediate buffer's non-ghost contents are undefined
+ * afterwards.  Bit-identical to `levels` sbp_iterate calls.  stamps: device
+ * array of sbp_fused_stamp_words(g) uint32, zero-filled once; epoch: a
+ * non-zero value never used before with this stamps array.  Band potentials,
+ * Ms >= 32, R <= 16; otherwise SBP_EUNSUPPORTED. */
+SBP_API int sbp_fused_stamp_words(const sbp_grid *g);
+SBP_API int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                              float *msgs_a, float *msgs_b, int levels, int iteration,
+                              int flags, unsigned *stamps, unsigned epoch, int lag, int rounds,
+                              unsigned long long *err, void *stream);
+
 /* One canonical SEQUENTIAL sweep in place (the reference's default schedule,
  * bp.py:492-503 -> numba_kernels.py:274-407): passes L->R, R->L, T->B, B->T,
  * each a set of independent row / column chains updated in order.  Full grid.
@@ -138,8 +157,9 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
 SBP_API int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values,
                       float *msgs, int sweep, unsigned long long *err, void *stream);
 
-/* Name of the kernel instantiation sbp_iterate (sequential = 0) or sbp_sweep
- * (sequential = 1) would launch for this grid and potential. */
+/* Name of the kernel instantiation sbp_iterate (sequential = 0), sbp_sweep
+ * (sequential = 1) or sbp_iterate_fused (sequential = 2; falls back to the
+ * sbp_iterate name when no fused kernel exists) would launch. */
 SBP_API int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential,
                           char *buf, int len);
 

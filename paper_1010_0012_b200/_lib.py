@@ -8,9 +8,11 @@ missing or cannot be loaded, importing the engine raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libsbp.so"
+# SBP_LIB selects another in-tree build of the same C ABI (kernel A/B runs).
+LIB_PATH = Path(__file__).resolve().parent / os.environ.get("SBP_LIB", "libsbp.so")
 
 SBP_OK, SBP_EINVAL, SBP_ECUDA, SBP_EUNSUPPORTED = 0, -1, -2, -3
 SBP_SUM, SBP_MAX = 0, 1
@@ -63,6 +65,9 @@ _PROTOS = {
                                ctypes.c_double, _P, _P]),
     "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
                          _i, _i, _i, _i, _P, _P]),
+    "sbp_fused_stamp_words": (_i, [ctypes.POINTER(SbpGrid)]),
+    "sbp_iterate_fused": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
+                               _i, _i, _i, _P, ctypes.c_uint, _i, _i, _P, _P]),
     "sbp_sweep": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _i, _P,
                        _P]),
     "sbp_plan_name": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _i,

@@ -24,6 +24,10 @@
 
 #include "sbp_common.cuh"
 
+#ifndef SBP_BAND_FORM
+#define SBP_BAND_FORM 0
+#endif
+
 namespace sbp {
 
 struct BandArgs {
@@ -37,7 +41,20 @@ struct BandArgs {
     int pass;      // sequential mode: pass direction 0..3 (chain_kernel.cuh)
     float fbar[2];
     float w[2][2 * SBP_MAX_R + 1];
+    // Pair table for the packed band: wp[o][k] = (w(k-R-1), w(k-R-2)), with
+    // w(d) = pad (0 / -inf) for |d| > R, R the compiled radius (band_pairs()).
+    float2 wp[2][2 * SBP_MAX_R + 4];
 };
+
+// Fills BandArgs::wp from BandArgs::w for the compiled radius R.
+__host__ inline void band_pairs(BandArgs &a, int R, float pad) {
+    for (int o = 0; o < 2; ++o)
+        for (int k = 0; k < 2 * SBP_MAX_R + 4; ++k) {
+            const int d0 = k - R - 1, d1 = k - R - 2;
+            a.wp[o][k].x = (d0 >= -R && d0 <= R) ? a.w[o][d0 + R] : pad;
+            a.wp[o][k].y = (d1 >= -R && d1 <= R) ? a.w[o][d1 + R] : pad;
+        }
+}
 
 // Per-iteration view of the buffers: which buffer is read / written, the
 // first row of the range, the iteration index (error key) and whether the
@@ -133,16 +150,67 @@ __device__ __forceinline__ void two_sum(float a, float b, float &s, float &e) {
 }
 
 // h'[i] = (s[i] - c) + e[i] with c = max over the node's labels of s.
+// Pairs of labels use the packed FP32 ops (bit-identical to the scalar ones).
 template <int VL, int LP>
 __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const float (&e)[VL],
                                                   float (&h)[VL]) {
     float c = s[0];
+    int i0 = 1;
+    if (VL % 2 == 0 && VL > 1) { c = fmaxf(s[0], s[1]); i0 = 2; }
 #pragma unroll
-    for (int i = 1; i < VL; ++i) c = fmaxf(c, s[i]);
+    for (int i = i0; i + 1 < VL; i += 2) c = fmax3(c, s[i], s[i + 1]);
+    if ((VL - i0) % 2 == 1) c = fmaxf(c, s[VL - 1]);
     c = lanes_max<LP>(c);
     if (!isfinite(c)) c = 0.0f;
 #pragma unroll
-    for (int i = 0; i < VL; ++i) h[i] = (s[i] - c) + (isfinite(s[i]) ? e[i] : 0.0f);
+    for (int i = 0; i + 1 < VL; i += 2) {
+        float d0, d1;
+        sub2(d0, d1, s[i], s[i + 1], c, c);
+        add2(h[i], h[i + 1], d0, d1, isfinite(s[i]) ? e[i] : 0.0f,
+             isfinite(s[i + 1]) ? e[i + 1] : 0.0f);
+    }
+    if (VL % 2 == 1) h[VL - 1] = (s[VL - 1] - c) + (isfinite(s[VL - 1]) ? e[VL - 1] : 0.0f);
+}
+
+// Pairwise helpers over VL-label arrays (VL even).
+template <int VL>
+__device__ __forceinline__ void vmul(float (&r)[VL], const float (&a)[VL], const float (&b)[VL]) {
+#pragma unroll
+    for (int i = 0; i < VL; i += 2) mul2(r[i], r[i + 1], a[i], a[i + 1], b[i], b[i + 1]);
+}
+
+// (s, e) = TwoSum(a, b) label-wise
+template <int VL>
+__device__ __forceinline__ void vtwo_sum(const float (&a)[VL], const float (&b)[VL], float (&s)[VL],
+                                         float (&e)[VL]) {
+#pragma unroll
+    for (int i = 0; i < VL; i += 2)
+        two_sum2(a[i], a[i + 1], b[i], b[i + 1], s[i], s[i + 1], e[i], e[i + 1]);
+}
+
+// s += b error-free, the new error added to e0 into e: (s, e) = (s + b, e0 + err)
+template <int VL>
+__device__ __forceinline__ void vtwo_sum_acc(float (&s)[VL], const float (&b)[VL],
+                                             const float (&e0)[VL], float (&e)[VL]) {
+#pragma unroll
+    for (int i = 0; i < VL; i += 2) {
+        float t0, t1, x0, x1;
+        two_sum2(s[i], s[i + 1], b[i], b[i + 1], t0, t1, x0, x1);
+        s[i] = t0; s[i + 1] = t1;
+        add2(e[i], e[i + 1], e0[i], e0[i + 1], x0, x1);
+    }
+}
+
+// (s, e) = TwoSum(a, b) with e = e0 + err (a fresh sum from a prefix a + e0)
+template <int VL>
+__device__ __forceinline__ void vtwo_sum_from(const float (&a)[VL], const float (&e0)[VL],
+                                              const float (&b)[VL], float (&s)[VL], float (&e)[VL]) {
+#pragma unroll
+    for (int i = 0; i < VL; i += 2) {
+        float x0, x1;
+        two_sum2(a[i], a[i + 1], b[i], b[i + 1], s[i], s[i + 1], x0, x1);
+        add2(e[i], e[i + 1], e0[i], e0[i + 1], x0, x1);
+    }
 }
 
 // One outgoing direction: fast update + normalisation + store.
@@ -164,43 +232,68 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
 #pragma unroll
         for (int i = 0; i < VL; ++i) out[i] = base;
     } else {
-        float mx = h[0];
+        float mx = fmaxf(h[0], h[1]);
 #pragma unroll
-        for (int i = 1; i < VL; ++i) mx = fmaxf(mx, h[i]);
+        for (int i = 2; i < VL; i += 2) mx = fmax3(mx, h[i], h[i + 1]);
         mx = lanes_max<LP>(mx);
         const float base = a.floor_term ? a.fbar[O] + mx : -__builtin_huge_valf();
 #pragma unroll
         for (int i = 0; i < VL; ++i) out[i] = base;
     }
     // Band, streamed in ascending x_i: term (x_i = x0+t) reaches out[i] at d = t - i.
+    // Label pairs (out[i], out[i+1]) take the weights (w(d), w(d-1)) of the
+    // pair table in one packed op; taps outside |d| <= R carry the pad weight
+    // (0 / -inf), exact no-ops, so every pair op is unconditional.
     if (DOM == SBP_SUM) {
+#if SBP_BAND_FORM == 1
+        // d outer (ascending d is ascending x_i for every output), label pairs
+        // inner: one FFMA2 per pair and tap with the weight as a broadcast
+        // scalar, so the weights stay uniform operands
+        float hx[VL + 2 * R];
+#pragma unroll
+        for (int t = -R; t < VL + R; ++t) hx[t + R] = band_h<DOM, VL, LP, R>(h, t, j);
+#pragma unroll
+        for (int d = -R; d <= R; ++d)
+#pragma unroll
+            for (int i = 0; i < VL; i += 2)
+                fma2b(out[i], out[i + 1], hx[i + d + R], hx[i + d + R + 1], a.w[O][d + R]);
+#else
 #pragma unroll
         for (int t = -R; t < VL + R; ++t) {
             const float hv = band_h<DOM, VL, LP, R>(h, t, j);
 #pragma unroll
-            for (int i = 0; i < VL; ++i) {
+            for (int i = 0; i < VL; i += 2) {
                 const int d = t - i;
-                if (d < -R || d > R) continue;
-                out[i] = fmaf(a.w[O][d + R], hv, out[i]);
+                if (d < -R || d > R + 1) continue;
+                fma2(out[i], out[i + 1], a.wp[O][d + R + 1], hv);
             }
         }
+#endif
     } else {
         // two taps per FMNMX3 (the max is exact: any grouping gives the same bits)
 #pragma unroll
         for (int t = -R; t < VL + R; t += 2) {
+            const bool has1 = t + 1 < VL + R;
             const float hv0 = band_h<DOM, VL, LP, R>(h, t, j);
-            const float hv1 = t + 1 < VL + R ? band_h<DOM, VL, LP, R>(h, t + 1, j) : 0.0f;
+            const float hv1 = has1 ? band_h<DOM, VL, LP, R>(h, t + 1, j) : 0.0f;
 #pragma unroll
-            for (int i = 0; i < VL; ++i) {
+            for (int i = 0; i < VL; i += 2) {
                 const int d0 = t - i, d1 = t + 1 - i;
-                const bool in0 = d0 >= -R && d0 <= R;
-                const bool in1 = t + 1 < VL + R && d1 >= -R && d1 <= R;
-                if (in0 && in1)
-                    out[i] = fmax3(out[i], a.w[O][d0 + R] + hv0, a.w[O][d1 + R] + hv1);
-                else if (in0)
-                    out[i] = fmaxf(out[i], a.w[O][d0 + R] + hv0);
-                else if (in1)
-                    out[i] = fmaxf(out[i], a.w[O][d1 + R] + hv1);
+                const bool in0 = d0 >= -R && d0 <= R + 1;
+                const bool in1 = has1 && d1 >= -R && d1 <= R + 1;
+                float a0, a1, b0, b1;
+                if (in0) add2(a0, a1, a.wp[O][d0 + R + 1].x, a.wp[O][d0 + R + 1].y, hv0, hv0);
+                if (in1) add2(b0, b1, a.wp[O][d1 + R + 1].x, a.wp[O][d1 + R + 1].y, hv1, hv1);
+                if (in0 && in1) {
+                    out[i] = fmax3(out[i], a0, b0);
+                    out[i + 1] = fmax3(out[i + 1], a1, b1);
+                } else if (in0) {
+                    out[i] = fmaxf(out[i], a0);
+                    out[i + 1] = fmaxf(out[i + 1], a1);
+                } else if (in1) {
+                    out[i] = fmaxf(out[i], b0);
+                    out[i + 1] = fmaxf(out[i + 1], b1);
+                }
             }
         }
     }
@@ -219,20 +312,20 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
         ok = (s > 0.0f) && !isinf(s);
         const float inv = __frcp_rn(s);
 #pragma unroll
-        for (int i = 0; i < VL; ++i) out[i] *= inv;
+        for (int i = 0; i < VL; i += 2) mul2(out[i], out[i + 1], out[i], out[i + 1], inv, inv);
     } else {
         if (a.M < a.Ms) {
 #pragma unroll
             for (int i = 0; i < VL; ++i)
                 if (x0 + i >= a.M) out[i] = -__builtin_huge_valf();
         }
-        float mx = out[0];
+        float mx = fmaxf(out[0], out[1]);
 #pragma unroll
-        for (int i = 1; i < VL; ++i) mx = fmaxf(mx, out[i]);
+        for (int i = 2; i < VL; i += 2) mx = fmax3(mx, out[i], out[i + 1]);
         mx = lanes_max<LP>(mx);
         ok = isfinite(mx);
 #pragma unroll
-        for (int i = 0; i < VL; ++i) out[i] -= mx;
+        for (int i = 0; i < VL; i += 2) sub2(out[i], out[i + 1], out[i], out[i + 1], mx, mx);
     }
     return ok;
 }
@@ -266,28 +359,25 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const IterCtx
         // Exclusion products in the reference order: unary, then slots 0..3
         // ascending, skipping the excluded one (numba_kernels.py:194-227).
         float ab[VL];
-#pragma unroll
-        for (int i = 0; i < VL; ++i) ab[i] = g[i] * m0[i];                  // g m0
+        vmul(ab, g, m0);                                                     // g m0
         if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
-#pragma unroll
-            for (int i = 0; i < VL; ++i) h[i] = ((g[i] * m1[i]) * m2[i]) * m3[i];
+            vmul(h, g, m1);
+            vmul(h, h, m2);
+            vmul(h, h, m3);
             emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, it, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
-#pragma unroll
-            for (int i = 0; i < VL; ++i) h[i] = (ab[i] * m2[i]) * m3[i];
+            vmul(h, ab, m2);
+            vmul(h, h, m3);
             emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, it, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
-#pragma unroll
-        for (int i = 0; i < VL; ++i) ab[i] = ab[i] * m1[i];                 // g m0 m1
+        vmul(ab, ab, m1);                                                    // g m0 m1
         if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
-#pragma unroll
-            for (int i = 0; i < VL; ++i) h[i] = ab[i] * m3[i];
+            vmul(h, ab, m3);
             emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, it, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
-#pragma unroll
-            for (int i = 0; i < VL; ++i) h[i] = ab[i] * m2[i];
+            vmul(h, ab, m2);
             emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, it, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     } else {
@@ -298,49 +388,28 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const IterCtx
         // up to ~2^-48 relative), shifted by the node's max of s, and only
         // then rounded: h' = (s - c) + e.  Messages are shift-invariant.
         float sa[VL], ea[VL], s2[VL], e2[VL];
-#pragma unroll
-        for (int i = 0; i < VL; ++i) two_sum(g[i], m0[i], sa[i], ea[i]);    // g + m0
+        vtwo_sum(g, m0, sa, ea);                                             // g + m0
         if (__any_sync(SBP_FULL_MASK, valid && has_u)) {                     // excl 0
-#pragma unroll
-            for (int i = 0; i < VL; ++i) {
-                float t, e;
-                two_sum(g[i], m1[i], s2[i], e2[i]);
-                two_sum(s2[i], m2[i], t, e); s2[i] = t; e2[i] += e;
-                two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
-            }
+            vtwo_sum(g, m1, s2, e2);
+            vtwo_sum_acc(s2, m2, e2, e2);
+            vtwo_sum_acc(s2, m3, e2, e2);
             shift_compensated<VL, LP>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, it, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
-#pragma unroll
-            for (int i = 0; i < VL; ++i) {
-                float t, e;
-                two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
-                two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
-            }
+            vtwo_sum_from(sa, ea, m2, s2, e2);
+            vtwo_sum_acc(s2, m3, e2, e2);
             shift_compensated<VL, LP>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, it, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
-#pragma unroll
-        for (int i = 0; i < VL; ++i) {                                       // g + m0 + m1
-            float t, e;
-            two_sum(sa[i], m1[i], t, e); sa[i] = t; ea[i] += e;
-        }
+        vtwo_sum_acc(sa, m1, ea, ea);                                        // g + m0 + m1
         if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
-#pragma unroll
-            for (int i = 0; i < VL; ++i) {
-                float e;
-                two_sum(sa[i], m3[i], s2[i], e); e2[i] = ea[i] + e;
-            }
+            vtwo_sum_from(sa, ea, m3, s2, e2);
             shift_compensated<VL, LP>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, it, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
-#pragma unroll
-            for (int i = 0; i < VL; ++i) {
-                float e;
-                two_sum(sa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
-            }
+            vtwo_sum_from(sa, ea, m2, s2, e2);
             shift_compensated<VL, LP>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, it, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
@@ -434,18 +503,12 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, const IterC
     // prefixes shared by the directions (same association as the unrolled
     // kernel, so both variants give identical bits)
     float pa[VL], pb[VL], ea[VL], eb[VL];
-#pragma unroll
-    for (int i = 0; i < VL; ++i) {
-        if (DOM == SBP_SUM) {
-            pa[i] = g[i] * m0[i];
-            pb[i] = pa[i] * m1[i];
-        } else {
-            float t, e;
-            two_sum(g[i], m0[i], pa[i], ea[i]);
-            two_sum(pa[i], m1[i], t, e);
-            pb[i] = t;
-            eb[i] = ea[i] + e;
-        }
+    if (DOM == SBP_SUM) {
+        vmul(pa, g, m0);
+        vmul(pb, pa, m1);
+    } else {
+        vtwo_sum(g, m0, pa, ea);
+        vtwo_sum_from(pa, ea, m1, pb, eb);
     }
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
@@ -454,27 +517,31 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, const IterC
         if (!__any_sync(SBP_FULL_MASK, valid && hd)) continue;
         float h[VL];
         if (DOM == SBP_SUM) {
-#pragma unroll
-            for (int i = 0; i < VL; ++i)
-                h[i] = dir == 3 ? ((g[i] * m1[i]) * m2[i]) * m3[i]
-                     : dir == 1 ? (pa[i] * m2[i]) * m3[i]
-                     : dir == 0 ? pb[i] * m3[i] : pb[i] * m2[i];
+            if (dir == 3) {
+                vmul(h, g, m1);
+                vmul(h, h, m2);
+                vmul(h, h, m3);
+            } else if (dir == 1) {
+                vmul(h, pa, m2);
+                vmul(h, h, m3);
+            } else if (dir == 0) {
+                vmul(h, pb, m3);
+            } else {
+                vmul(h, pb, m2);
+            }
         } else {
             float s2[VL], e2[VL];
-#pragma unroll
-            for (int i = 0; i < VL; ++i) {
-                float t, e;
-                if (dir == 3) {
-                    two_sum(g[i], m1[i], s2[i], e2[i]);
-                    two_sum(s2[i], m2[i], t, e); s2[i] = t; e2[i] += e;
-                    two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
-                } else if (dir == 1) {
-                    two_sum(pa[i], m2[i], s2[i], e); e2[i] = ea[i] + e;
-                    two_sum(s2[i], m3[i], t, e); s2[i] = t; e2[i] += e;
-                } else {
-                    two_sum(pb[i], dir == 0 ? m3[i] : m2[i], s2[i], e);
-                    e2[i] = eb[i] + e;
-                }
+            if (dir == 3) {
+                vtwo_sum(g, m1, s2, e2);
+                vtwo_sum_acc(s2, m2, e2, e2);
+                vtwo_sum_acc(s2, m3, e2, e2);
+            } else if (dir == 1) {
+                vtwo_sum_from(pa, ea, m2, s2, e2);
+                vtwo_sum_acc(s2, m3, e2, e2);
+            } else if (dir == 0) {
+                vtwo_sum_from(pb, eb, m3, s2, e2);
+            } else {
+                vtwo_sum_from(pb, eb, m2, s2, e2);
             }
             shift_compensated<VL, LP>(s2, e2, h);
         }
@@ -699,7 +766,7 @@ BandLaunchFn pick_band_r(int R) {
         switch (R) {
 #define SBP_CASE(RR)                                                      \
     case RR:                                                              \
-        if constexpr (RR < MS && (!ROLLED || RR >= 24) &&                   \
+        if constexpr (RR < MS && (!ROLLED || RR >= 24 || RR == 7 || RR == 8 || RR == 4) && \
                       (VL == 8 || ROLLED || RR <= 8))                         \
             return &launch_band<DOM, VL, MS / VL, RR, ROLLED>;             \
         else return nullptr;

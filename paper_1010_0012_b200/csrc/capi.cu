@@ -6,6 +6,7 @@
 
 #include "aux_kernels.cuh"
 #include "band_kernel.cuh"
+#include "fused_kernel.cuh"
 
 namespace sbp {
 template <int MS, int DOM>
@@ -20,6 +21,14 @@ BandLaunchFn pick_band(int dom, int vl, int R, int rolled) {
 namespace sbp {
 template <int MS, int DOM>
 BandLaunchFn pick_chain(int R);
+// instantiated in band_ms*_*.cu (keeps this file from compiling every kernel)
+#define SBP_EXTERN(MSV)                                                          \
+    extern template BandLaunchFn pick_band_dom<MSV, SBP_SUM>(int, int, int);      \
+    extern template BandLaunchFn pick_band_dom<MSV, SBP_MAX>(int, int, int);      \
+    extern template FusedLaunchFn pick_fused<MSV, SBP_SUM>(int);                 \
+    extern template FusedLaunchFn pick_fused<MSV, SBP_MAX>(int);
+SBP_EXTERN(8) SBP_EXTERN(16) SBP_EXTERN(32) SBP_EXTERN(64) SBP_EXTERN(128) SBP_EXTERN(256)
+#undef SBP_EXTERN
 }
 
 namespace {
@@ -88,7 +97,11 @@ int band_roll_min_r() {
 
 BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
     BandChoice c;
-    if (sym && Rk >= 24 && Rk >= band_roll_min_r()) {
+    // packed-FP32 build, B200 A/B (profiles/r01_ab_packed.txt): the rolled
+    // VL=16 kernel is the fastest for C4 (sum, Ms=128, R=7) cold and
+    // sustained; rolled instantiations exist for R in {4, 7, 8} and R >= 24
+    const bool rolled_c4 = sym && domain == SBP_SUM && Ms == 128 && (Rk == 4 || Rk == 7 || Rk == 8);
+    if ((sym && Rk >= band_roll_min_r()) || (rolled_c4 && env_int("SBP_ROLL_MIN_R", 0) != 99)) {
         c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
         c.variant = 1;
     } else {
@@ -151,6 +164,37 @@ sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled) {
     case 256: return sbp::pick_band<256>(dom, vl, R, rolled);
     default: return nullptr;
     }
+}
+
+// Geometry and band weights (compiled radius Rk) of a band launch.
+void band_args(const sbp_grid *g, const sbp_potential *pot, int Rk, const float *values,
+               sbp::BandArgs *a) {
+    memset(a, 0, sizeof *a);
+    a->values = values;
+    a->slot_stride = (long long)(g->rows + 2) * g->W * g->Ms;
+    a->H = g->H; a->W = g->W; a->M = g->M; a->Ms = g->Ms; a->r0 = g->r0;
+    a->floor_term = pot->floor_term;
+    const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    for (int o = 0; o < 2; ++o) {
+        a->fbar[o] = pot->fbar[o];
+        for (int k = 0; k < 2 * SBP_MAX_R + 1; ++k) a->w[o][k] = pad;
+        for (int d = -pot->R; d <= pot->R; ++d) a->w[o][d + Rk] = pot->band_w[o][d + pot->R];
+    }
+    sbp::band_pairs(*a, Rk, pad);
+}
+
+int band_radius(const sbp_grid *g, const sbp_potential *pot) {
+    for (int r : kRadii)
+        if (r >= pot->R && r < g->Ms) return r;
+    return 0;
+}
+
+sbp::FusedLaunchFn fused_fn(int Ms, int dom, int R) {
+#define SBP_F(MSV)                                                                        \
+    case MSV:                                                                             \
+        return dom == SBP_SUM ? sbp::pick_fused<MSV, SBP_SUM>(R) : sbp::pick_fused<MSV, SBP_MAX>(R);
+    switch (Ms) { SBP_F(8) SBP_F(16) SBP_F(32) SBP_F(64) SBP_F(128) SBP_F(256) default: return nullptr; }
+#undef SBP_F
 }
 
 int ell_args(const sbp_grid *g, const sbp_potential *pot, sbp::EllArgs *a) {
@@ -250,21 +294,12 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         if (!fn)
             return fail(SBP_EUNSUPPORTED, "no band kernel for Ms=%d R=%d", g->Ms, pot->R);
         sbp::BandArgs a;
-        a.values = values;
+        band_args(g, pot, Rk, values, &a);
         a.msgs_in = msgs_in;
         a.msgs_out = msgs_out;
         a.err = err;
-        a.slot_stride = slot;
-        a.H = g->H; a.W = g->W; a.M = g->M; a.Ms = g->Ms; a.r0 = g->r0;
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
-        a.floor_term = pot->floor_term;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
-        const float pad = pot->domain == SBP_SUM ? 0.0f : -__builtin_huge_valf();
-        for (int o = 0; o < 2; ++o) {
-            a.fbar[o] = pot->fbar[o];
-            for (int k = 0; k < 2 * SBP_MAX_R + 1; ++k) a.w[o][k] = pad;
-            for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
-        }
         return cuda_status(fn(a, s), "sbp_iterate(band)");
     }
     if (pot->kind == SBP_POT_DENSE && pot->n_pot == 0 && pot->dense_t[0] && pot->dense_t[1] &&
@@ -294,6 +329,53 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         return cuda_status(sbp::launch_ell(pot->domain, a, s), "sbp_iterate(ell)");
     }
     return fail(SBP_EINVAL, "unknown potential kind %d", pot->kind);
+}
+
+int sbp_fused_stamp_words(const sbp_grid *g) {
+    if (int rc = check_grid(g)) return rc;
+    return sbp::SBP_FUSE_MAX * g->rows * ((g->W + 3) / 4);   // segments >= 4 pixels
+}
+
+int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                      float *msgs_a, float *msgs_b, int levels, int iteration, int flags,
+                      unsigned *stamps, unsigned epoch, int lag, int rounds,
+                      unsigned long long *err, void *stream) {
+    if (int rc = check_grid(g)) return rc;
+    if (!pot || !values || !msgs_a || !msgs_b || !stamps || !err)
+        return fail(SBP_EINVAL, "NULL pointer");
+    if (levels < 1 || levels > sbp::SBP_FUSE_MAX)
+        return fail(SBP_EINVAL, "levels must be in [1, %d]", sbp::SBP_FUSE_MAX);
+    if (lag < 2 || rounds < 1) return fail(SBP_EINVAL, "lag must be >= 2 and rounds >= 1");
+    if (epoch == 0) return fail(SBP_EINVAL, "epoch 0 is the cleared stamp value");
+    if (iteration < 0 || iteration + levels > (1 << 23)) return fail(SBP_EINVAL, "bad iteration index");
+    if (pot->kind != SBP_POT_BAND || pot->domain != SBP_SUM && pot->domain != SBP_MAX)
+        return fail(SBP_EUNSUPPORTED, "fused iterations need a band potential");
+    if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
+    const int Rk = band_radius(g, pot);
+    sbp::FusedLaunchFn fn = Rk ? fused_fn(g->Ms, pot->domain, Rk) : nullptr;
+    if (!fn) return fail(SBP_EUNSUPPORTED, "no fused kernel for Ms=%d R=%d", g->Ms, pot->R);
+    select_device_of(msgs_a);
+    sbp::BandArgs a;
+    band_args(g, pot, Rk, values, &a);
+    a.err = err;
+    a.lr_begin = 1;
+    a.lr_end = g->rows + 1;
+    sbp::FusedArgs f;
+    memset(&f, 0, sizeof f);
+    float *buf[2] = {msgs_a, msgs_b};
+    for (int l = 0; l < levels; ++l) {
+        f.lev[l].msgs_in = buf[l & 1];
+        f.lev[l].msgs_out = buf[(l + 1) & 1];
+        f.lev[l].lr_begin = 1;
+        f.lev[l].iteration = iteration + l;
+        f.lev[l].first = (l == 0 && (flags & SBP_ITER_FIRST)) ? 1 : 0;
+    }
+    f.stamps = stamps;
+    f.epoch = epoch;
+    f.T = levels;
+    f.D = lag;
+    f.rounds = rounds;
+    return cuda_status(fn(a, f, (cudaStream_t)stream), "sbp_iterate_fused");
 }
 
 int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, float *msgs,
@@ -345,6 +427,7 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
         for (int k = 0; k < 2 * SBP_MAX_R + 1; ++k) a.w[o][k] = pad;
         for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
     }
+    sbp::band_pairs(a, Rk, pad);
     return cuda_status(fn(a, (cudaStream_t)stream), "sbp_sweep");
 }
 
@@ -357,8 +440,11 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         int Rk = 0;
         for (int r : kRadii)
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
-        if (sequential) {
+        if (sequential == 1) {
             snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
+        } else if (sequential == 2 && Rk && fused_fn(g->Ms, pot->domain, Rk)) {
+            const int vl = (pot->domain == SBP_SUM && g->Ms >= 128 && Rk <= 8) ? 16 : 8;
+            snprintf(buf, len, "band_fused_kernel<%s,VL=%d,LP=%d,R=%d>", dom, vl, g->Ms / vl, Rk);
         } else {
             BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
             if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);

@@ -45,17 +45,14 @@ __device__ __forceinline__ void chain_h(const float (&g)[VL], const float (&ma)[
     // the three included slots in ascending order are (ma, mb, mc); see
     // chain_pass_kernel for the assignment per pass
     if (DOM == SBP_SUM) {
-#pragma unroll
-        for (int i = 0; i < VL; ++i) h[i] = ((g[i] * ma[i]) * mb[i]) * mc[i];
+        vmul(h, g, ma);
+        vmul(h, h, mb);
+        vmul(h, h, mc);
     } else {
         float s[VL], e[VL];
-#pragma unroll
-        for (int i = 0; i < VL; ++i) {
-            float t, ee;
-            two_sum(g[i], ma[i], s[i], e[i]);
-            two_sum(s[i], mb[i], t, ee); s[i] = t; e[i] += ee;
-            two_sum(s[i], mc[i], t, ee); s[i] = t; e[i] += ee;
-        }
+        vtwo_sum(g, ma, s, e);
+        vtwo_sum_acc(s, mb, e, e);
+        vtwo_sum_acc(s, mc, e, e);
         shift_compensated<VL, LP>(s, e, h);
     }
 }

@@ -42,6 +42,85 @@ __host__ __device__ constexpr int dir_excl(int d) { return d == 0 ? 2 : d == 1 ?
 __host__ __device__ constexpr int dir_wslot(int d) { return d == 0 ? 1 : d == 1 ? 2 : d == 2 ? 0 : 3; }
 __host__ __device__ constexpr int dir_orient(int d) { return (d == 0 || d == 2) ? 0 : 1; }
 
+// Packed FP32 pairs (sm_100 FADD2 / FMUL2 / FFMA2).  Each half rounds exactly
+// like the scalar instruction (IEEE round-to-nearest, no contraction), so a
+// packed loop gives the same bits as the scalar one with half the issue slots.
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float &a, float &b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+
+#ifndef SBP_SCALAR_F32
+// (r0, r1) = (a0 + b0, a1 + b1)
+__device__ __forceinline__ void add2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a0, a1)), "l"(f2_pack(b0, b1)));
+    f2_unpack(r, r0, r1);
+}
+
+// (r0, r1) = (a0 - b0, a1 - b1)
+__device__ __forceinline__ void sub2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a0, a1)), "l"(f2_pack(b0, b1)));
+    f2_unpack(r, r0, r1);
+}
+
+// (r0, r1) = (a0 * b0, a1 * b1)
+__device__ __forceinline__ void mul2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a0, a1)), "l"(f2_pack(b0, b1)));
+    f2_unpack(r, r0, r1);
+}
+
+// (o0, o1) = (fma(w.x, x, o0), fma(w.y, x, o1))
+__device__ __forceinline__ void fma2(float &o0, float &o1, float2 w, float x) {
+    unsigned long long r = f2_pack(o0, o1);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(f2_pack(w.x, w.y)), "l"(f2_pack(x, x)));
+    f2_unpack(r, o0, o1);
+}
+
+// (o0, o1) = (fma(x0, w, o0), fma(x1, w, o1)): one weight for a label pair
+__device__ __forceinline__ void fma2b(float &o0, float &o1, float x0, float x1, float w) {
+    unsigned long long r = f2_pack(o0, o1);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(f2_pack(x0, x1)), "l"(f2_pack(w, w)));
+    f2_unpack(r, o0, o1);
+}
+#else
+// Scalar build (A/B comparisons only): the same roundings one lane at a time.
+__device__ __forceinline__ void add2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    r0 = __fadd_rn(a0, b0); r1 = __fadd_rn(a1, b1);
+}
+__device__ __forceinline__ void sub2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    r0 = __fsub_rn(a0, b0); r1 = __fsub_rn(a1, b1);
+}
+__device__ __forceinline__ void mul2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    r0 = __fmul_rn(a0, b0); r1 = __fmul_rn(a1, b1);
+}
+__device__ __forceinline__ void fma2(float &o0, float &o1, float2 w, float x) {
+    o0 = fmaf(w.x, x, o0); o1 = fmaf(w.y, x, o1);
+}
+__device__ __forceinline__ void fma2b(float &o0, float &o1, float x0, float x1, float w) {
+    o0 = fmaf(x0, w, o0); o1 = fmaf(x1, w, o1);
+}
+#endif
+
+// Knuth TwoSum on a pair: a + b = s + e exactly, per half (adds only).
+__device__ __forceinline__ void two_sum2(float a0, float a1, float b0, float b1, float &s0,
+                                         float &s1, float &e0, float &e1) {
+    float bp0, bp1, t0, t1, u0, u1, v0, v1;
+    add2(s0, s1, a0, a1, b0, b1);
+    sub2(bp0, bp1, s0, s1, a0, a1);
+    sub2(t0, t1, s0, s1, bp0, bp1);
+    sub2(u0, u1, a0, a1, t0, t1);
+    sub2(v0, v1, b0, b1, bp0, bp1);
+    add2(e0, e1, u0, u1, v0, v1);
+}
+
 __device__ __forceinline__ float4 ldg_stream(const float4 *p) {
     float4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"

@@ -27,6 +27,7 @@ kernels, ``csrc/``); torch provides device memory, streams and events only.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass, field
 
@@ -221,6 +222,16 @@ class GridEngine:
             self.upload_values(values)
         for buf in self.msgs:
             self._init(buf, ghosts_only=True)
+        # temporal blocking (sbp_iterate_fused): up to `fuse` synchronous
+        # iterations per launch on a whole single-GPU grid; SBP_FUSE=1 turns
+        # it off.  Lag (rows between levels) and rounds (pixel groups per
+        # warp and work unit) are tuning knobs of the wavefront.
+        self.fuse = int(os.environ.get("SBP_FUSE", "1"))
+        self.fuse_lag = int(os.environ.get("SBP_FUSE_LAG", "3"))
+        self.fuse_rounds = int(os.environ.get("SBP_FUSE_ROUNDS", "1"))
+        self._fused_ok: bool | None = None
+        self._stamps: torch.Tensor | None = None
+        self._epoch = 0
         self.reset()
 
     # -- setup -------------------------------------------------------------
@@ -298,8 +309,9 @@ class GridEngine:
             return "none"
         import ctypes
         buf = ctypes.create_string_buffer(128)
+        mode = 1 if self.schedule == SEQUENTIAL else (2 if self._can_fuse() else 0)
         L.check(self.lib.sbp_plan_name(ctypes_ref(self.grid), ctypes_ref(self._pot_struct),
-                                       1 if self.schedule == SEQUENTIAL else 0, buf, 128))
+                                       mode, buf, 128))
         return buf.value.decode()
 
     def _init(self, buf: torch.Tensor, ghosts_only: bool) -> None:
@@ -348,6 +360,35 @@ class GridEngine:
         self.cur = 1 - self.cur
         self.iterations += 1
 
+    def _can_fuse(self) -> bool:
+        return (self.fuse >= 2 and self._fused_ok is not False
+                and self.schedule == SYNCHRONOUS and self.plan is not None
+                and self.plan.kind == L.SBP_POT_BAND and self.Ms >= 32
+                and self.r0 == 0 and self.rows == self.H)
+
+    def iterate_fused(self, levels: int) -> bool:
+        """`levels` synchronous iterations in one temporally blocked launch
+        (bit-identical to `levels` iterate_rows + flip).  Returns False, with
+        nothing launched, when no fused kernel exists for this plan."""
+        if self._stamps is None:
+            words = self.lib.sbp_fused_stamp_words(ctypes_ref(self.grid))
+            L.check(min(words, 0))
+            self._stamps = torch.zeros(words, dtype=torch.int32, device=self.device)
+        self._epoch += 1
+        rc = self.lib.sbp_iterate_fused(
+            ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
+            _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), levels, self.iterations,
+            L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self._stamps), self._epoch,
+            self.fuse_lag, self.fuse_rounds, _ptr(self.err), _stream_handle())
+        if rc == L.SBP_EUNSUPPORTED:
+            self._fused_ok = False
+            return False
+        L.check(rc)
+        self._fused_ok = True
+        self.cur = (self.cur + levels) % 2
+        self.iterations += levels
+        return True
+
     def sweep(self) -> None:
         """One canonical sequential sweep in place (reference ``_run_grid``)."""
         if self.plan is not None:
@@ -371,18 +412,23 @@ class GridEngine:
                 if events is not None:
                     ev1 = torch.cuda.Event(enable_timing=True)
                     ev1.record()
-                    events.append((ev0, ev1))
+                    events.append((ev0, ev1, 1))
             return
-        for _ in range(n):
+        done = 0
+        while done < n:
+            k = min(self.fuse, n - done) if self._can_fuse() else 1
             if events is not None:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            self.iterate_rows(1, self.rows + 1)
-            self.flip()
+            if k < 2 or not self.iterate_fused(k):
+                k = 1
+                self.iterate_rows(1, self.rows + 1)
+                self.flip()
             if events is not None:
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev1.record()
-                events.append((ev0, ev1))
+                events.append((ev0, ev1, k))
+            done += k
 
     def max_abs_delta(self) -> float:
         out = torch.zeros(1, dtype=torch.float32, device=self.device)
@@ -571,18 +617,24 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
         eng.reset(full=convergence_tol is not None)
     per_iter = 2 * int(model.n_edges)
     events: list = []
-    for _ in range(n_sweeps):
-        if mode == SEQUENTIAL and convergence_tol is not None:
-            eng.snapshot()
-        eng.step(1, events=events)
-        stats.sweeps_run += 1
-        stats.n_updates += per_iter
-        if convergence_tol is not None:
+    if convergence_tol is None:
+        # no per-sweep test: the engine may fuse iterations into one launch
+        eng.step(n_sweeps, events=events)
+        stats.sweeps_run += n_sweeps
+        stats.n_updates += per_iter * n_sweeps
+    else:
+        for _ in range(n_sweeps):
+            if mode == SEQUENTIAL:
+                eng.snapshot()
+            eng.step(1, events=events)
+            stats.sweeps_run += 1
+            stats.n_updates += per_iter
             if eng.max_abs_delta() < convergence_tol:
                 stats.converged = True
                 break
     torch.cuda.synchronize(eng.device)
-    stats.sweep_seconds = [a.elapsed_time(b) / 1e3 for a, b in events]
+    # per-sweep device seconds (a fused launch of k iterations counts k equal shares)
+    stats.sweep_seconds = [a.elapsed_time(b) / 1e3 / k for a, b, k in events for _ in range(k)]
     if eng.plan.madds_per_sweep is not None:
         stats.madds = eng.plan.madds_per_sweep * stats.sweeps_run
     else:

@@ -223,7 +223,7 @@ def _plan_name(cfg_name, domain, sequential=False):
 
 
 @pytest.mark.parametrize("name,domain,expect", [
-    ("C4", "sum", "band_iter_kernel<sum,VL=16,LP=8,R=7>"),
+    ("C4", "sum", "band_iter_kernel<sum,VL=16,LP=8,R=7,rolled>"),
     ("C3", "max", "band_iter_staged_kernel<max,VL=8,LP=8,R=3>"),
     ("C2", "sum", "band_iter_kernel<sum,VL=8,LP=4,R=2>"),
     ("C5_T5", "sum", "band_iter_staged_kernel<sum,VL=16,LP=16,R=4>"),
@@ -241,6 +241,8 @@ def test_plan_name_reports_the_fallback(monkeypatch):
     monkeypatch.setenv("SBP_STAGED", "0")
     monkeypatch.setenv("SBP_BAND_VL", "16")
     assert _plan_name("C5_T17", "sum") == "band_iter_kernel<sum,VL=8,LP=32,R=16>"
-    assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=16,LP=8,R=7>"
+    assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=16,LP=8,R=7,rolled>"
     monkeypatch.setenv("SBP_BAND_VL", "8")
+    assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=8,LP=16,R=7,rolled>"
+    monkeypatch.setenv("SBP_ROLL_MIN_R", "99")
     assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=8,LP=16,R=7>"

@@ -38,7 +38,7 @@ for T in (2, 5, 9, 17, 33):
             evs = []
             eng.step(iters, events=evs)
             torch.cuda.synchronize()
-            ms = sorted(a.elapsed_time(b) for a, b in evs[1:] or evs)[len(evs[1:] or evs) // 2]
+            ms = sorted(a.elapsed_time(b) / k for a, b, k in evs[1:] or evs)[len(evs[1:] or evs) // 2]
             F = E * 2 * ((pot.nnz + 2 * M) if kernel == "fast" else M * M)
             res[kernel] = {"ms_per_iter": ms, "updates_per_s": E / ms * 1e3,
                            "hbm_frac": B / ms / 1e6 / peak,

@@ -24,7 +24,7 @@ torch.cuda.synchronize()
 evs = []
 eng.step(iters, events=evs)
 torch.cuda.synchronize()
-ms = [a.elapsed_time(b) for a, b in evs]
+ms = [a.elapsed_time(b) / k for a, b, k in evs]
 steady = sorted(ms)[len(ms) // 2]
 H, W, M = cfg.height, cfg.width, cfg.M
 B = 4 * M * (H * W + 2 * cfg.n_directed)

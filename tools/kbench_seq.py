@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 evs = []
 eng.step(sweeps, events=evs)
 torch.cuda.synchronize()
-ms = sorted(a.elapsed_time(b) for a, b in evs)[len(evs) // 2]
+ms = sorted(a.elapsed_time(b) for a, b, _ in evs)[len(evs) // 2]
 H, W, M = cfg.height, cfg.width, cfg.M
 N = H * W
 # per sweep: every directed message written once; per update the unary and two
