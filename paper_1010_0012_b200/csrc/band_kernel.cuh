@@ -457,6 +457,14 @@ __device__ __forceinline__ void band_group(const BandArgs &a, const IterCtx &it,
     band_group_body<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
 }
 
+template <int DOM, int VL, int LP, int R>
+__device__ __forceinline__ void band_group_body_rolled(const BandArgs &a, const IterCtx &it,
+                                                       const float (&g)[VL],
+                                                       const float (&m0)[VL], const float (&m1)[VL],
+                                                       const float (&m2)[VL], const float (&m3)[VL],
+                                                       int j, int x0, bool valid, long long node_l,
+                                                       long long r, int c);
+
 // Rolled variant for potentials whose two orientations carry the same band
 // (symmetric f, e.g. every truncated-linear / quadratic config): one copy of
 // the fully unrolled band serves all four directions (runtime loop), cutting
@@ -496,6 +504,17 @@ __device__ __forceinline__ void band_group_rolled(const BandArgs &a, const IterC
                 mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
         }
     }
+    band_group_body_rolled<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
+}
+
+// The four messages of one node, one band copy for all four directions.
+template <int DOM, int VL, int LP, int R>
+__device__ __forceinline__ void band_group_body_rolled(const BandArgs &a, const IterCtx &it,
+                                                       const float (&g)[VL],
+                                                       const float (&m0)[VL], const float (&m1)[VL],
+                                                       const float (&m2)[VL], const float (&m3)[VL],
+                                                       int j, int x0, bool valid, long long node_l,
+                                                       long long r, int c) {
     // bit d: the node has a neighbour in direction d (no local arrays:
     // runtime-indexed arrays would live in local memory)
     const unsigned has = (c + 1 < a.W ? 1u : 0u) | (c > 0 ? 2u : 0u) |

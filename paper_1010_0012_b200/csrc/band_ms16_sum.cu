@@ -2,5 +2,5 @@
 #include "fused_kernel.cuh"
 namespace sbp {
 template BandLaunchFn pick_band_dom<16, SBP_SUM>(int, int, int);
-template FusedLaunchFn pick_fused<16, SBP_SUM>(int);
+template FusedLaunchFn pick_fused<16, SBP_SUM>(int, bool);
 }

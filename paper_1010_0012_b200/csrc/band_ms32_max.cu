@@ -2,5 +2,5 @@
 #include "fused_kernel.cuh"
 namespace sbp {
 template BandLaunchFn pick_band_dom<32, SBP_MAX>(int, int, int);
-template FusedLaunchFn pick_fused<32, SBP_MAX>(int);
+template FusedLaunchFn pick_fused<32, SBP_MAX>(int, bool);
 }

@@ -25,8 +25,8 @@ BandLaunchFn pick_chain(int R);
 #define SBP_EXTERN(MSV)                                                          \
     extern template BandLaunchFn pick_band_dom<MSV, SBP_SUM>(int, int, int);      \
     extern template BandLaunchFn pick_band_dom<MSV, SBP_MAX>(int, int, int);      \
-    extern template FusedLaunchFn pick_fused<MSV, SBP_SUM>(int);                 \
-    extern template FusedLaunchFn pick_fused<MSV, SBP_MAX>(int);
+    extern template FusedLaunchFn pick_fused<MSV, SBP_SUM>(int, bool);           \
+    extern template FusedLaunchFn pick_fused<MSV, SBP_MAX>(int, bool);
 SBP_EXTERN(8) SBP_EXTERN(16) SBP_EXTERN(32) SBP_EXTERN(64) SBP_EXTERN(128) SBP_EXTERN(256)
 #undef SBP_EXTERN
 }
@@ -189,12 +189,21 @@ int band_radius(const sbp_grid *g, const sbp_potential *pot) {
     return 0;
 }
 
-sbp::FusedLaunchFn fused_fn(int Ms, int dom, int R) {
+sbp::FusedLaunchFn fused_fn(int Ms, int dom, int R, bool rolled) {
 #define SBP_F(MSV)                                                                        \
     case MSV:                                                                             \
-        return dom == SBP_SUM ? sbp::pick_fused<MSV, SBP_SUM>(R) : sbp::pick_fused<MSV, SBP_MAX>(R);
+        return dom == SBP_SUM ? sbp::pick_fused<MSV, SBP_SUM>(R, rolled)                   \
+                              : sbp::pick_fused<MSV, SBP_MAX>(R, rolled);
     switch (Ms) { SBP_F(8) SBP_F(16) SBP_F(32) SBP_F(64) SBP_F(128) SBP_F(256) default: return nullptr; }
 #undef SBP_F
+}
+
+// Rolled fused body: symmetric band with a compiled rolled instantiation
+// (SBP_FUSE_ROLLED=0 forces the unrolled one).
+bool fused_rolled(const sbp_grid *g, const sbp_potential *pot, int Rk) {
+    (void)g;
+    return (Rk == 4 || Rk == 7 || Rk == 8) && band_symmetric(pot) &&
+           env_int("SBP_FUSE_ROLLED", 1) != 0;
 }
 
 int ell_args(const sbp_grid *g, const sbp_potential *pot, sbp::EllArgs *a) {
@@ -333,7 +342,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
 
 int sbp_fused_stamp_words(const sbp_grid *g) {
     if (int rc = check_grid(g)) return rc;
-    return sbp::SBP_FUSE_MAX * g->rows * ((g->W + 3) / 4);   // segments >= 4 pixels
+    return sbp::SBP_FUSE_MAX * g->rows * g->W;   // units of >= 1 pixel
 }
 
 int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *values,
@@ -352,7 +361,7 @@ int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *
         return fail(SBP_EUNSUPPORTED, "fused iterations need a band potential");
     if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
     const int Rk = band_radius(g, pot);
-    sbp::FusedLaunchFn fn = Rk ? fused_fn(g->Ms, pot->domain, Rk) : nullptr;
+    sbp::FusedLaunchFn fn = Rk ? fused_fn(g->Ms, pot->domain, Rk, fused_rolled(g, pot, Rk)) : nullptr;
     if (!fn) return fail(SBP_EUNSUPPORTED, "no fused kernel for Ms=%d R=%d", g->Ms, pot->R);
     select_device_of(msgs_a);
     sbp::BandArgs a;
@@ -442,9 +451,10 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
         if (sequential == 1) {
             snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
-        } else if (sequential == 2 && Rk && fused_fn(g->Ms, pot->domain, Rk)) {
+        } else if (sequential == 2 && Rk && fused_fn(g->Ms, pot->domain, Rk, false)) {
             const int vl = (pot->domain == SBP_SUM && g->Ms >= 128 && Rk <= 8) ? 16 : 8;
-            snprintf(buf, len, "band_fused_kernel<%s,VL=%d,LP=%d,R=%d>", dom, vl, g->Ms / vl, Rk);
+            snprintf(buf, len, "band_fused_kernel<%s,VL=%d,LP=%d,R=%d%s>", dom, vl, g->Ms / vl, Rk,
+                     fused_rolled(g, pot, Rk) ? ",rolled" : "");
         } else {
             BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
             if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);

@@ -226,9 +226,9 @@ class GridEngine:
         # iterations per launch on a whole single-GPU grid; SBP_FUSE=1 turns
         # it off.  Lag (rows between levels) and rounds (pixel groups per
         # warp and work unit) are tuning knobs of the wavefront.
-        self.fuse = int(os.environ.get("SBP_FUSE", "1"))
-        self.fuse_lag = int(os.environ.get("SBP_FUSE_LAG", "3"))
-        self.fuse_rounds = int(os.environ.get("SBP_FUSE_ROUNDS", "1"))
+        self.fuse = _default_fuse(self.domain, self.Ms, self.plan)
+        self.fuse_lag = int(os.environ.get("SBP_FUSE_LAG", "4"))
+        self.fuse_rounds = int(os.environ.get("SBP_FUSE_ROUNDS", "2"))
         self._fused_ok: bool | None = None
         self._stamps: torch.Tensor | None = None
         self._epoch = 0
@@ -504,6 +504,21 @@ class GridEngine:
         """Reference-layout (4, N, M) f64 copy of the current messages."""
         cur = self.current[:, 1:self.rows + 1, :, :self.M]
         return cur.reshape(4, self.rows * self.W, self.M).double().cpu().numpy()
+
+
+def _default_fuse(domain: str, Ms: int, plan) -> int:
+    """Iterations per launch (SBP_FUSE overrides).  Temporal blocking halves
+    HBM traffic but adds per-unit synchronisation; on B200 it only wins where
+    the band is cheap and memory dominates (A/B, profiles/r01_ab_fused.md):
+    sum-product, Ms >= 256, R <= 2 (C5 T=2: 1.37 vs 1.58 ms per iteration).
+    Everywhere else (C4: 2.41-2.60 vs 2.32) one iteration per launch."""
+    env = os.environ.get("SBP_FUSE")
+    if env is not None:
+        return int(env)
+    if (domain == "sum" and Ms >= 256 and plan is not None
+            and plan.kind == L.SBP_POT_BAND and plan.R <= 2):
+        return 3
+    return 1
 
 
 def ctypes_ref(obj):

@@ -72,9 +72,10 @@ def test_fused_continues_from_previous_state():
     np.testing.assert_array_equal(eng.msgs4(), ref.msgs4())
 
 
-def test_run_sweeps_fuses_and_matches_oracle():
-    """The public API fuses iterations by default; results stay within the
-    oracle tolerance and the per-sweep stats have one entry per sweep."""
+def test_run_sweeps_fuses_and_matches_oracle(monkeypatch):
+    """With SBP_FUSE set the public API fuses iterations; results stay within
+    the oracle tolerance and the per-sweep stats have one entry per sweep."""
+    monkeypatch.setenv("SBP_FUSE", "3")
     model = synth.build_config_model(synth.CONFIGS["C4"], height=24, width=40)
     store = sbp.run_sweeps(model, 9, schedule="synchronous")
     assert store.engine._fused_ok
