@@ -24,8 +24,8 @@
 
 #include "sbp_common.cuh"
 
-#ifndef SBP_BAND_FORM
-#define SBP_BAND_FORM 0
+#ifndef SBP_HSMEM
+#define SBP_HSMEM 1   // out-of-lane band taps through shared memory (0: shuffles)
 #endif
 
 namespace sbp {
@@ -131,6 +131,64 @@ __device__ __forceinline__ float band_h(const float (&h)[VL], int t, int j) {
     float v = __shfl_down_sync(SBP_FULL_MASK, h[idx], q, LP);
     return j + q < LP ? v : PAD;
 }
+
+// The band's out-of-lane taps h(x0 + t), t in [-R, 0) and [VL, VL + R): the
+// neighbouring lanes' labels of the same node, or the pad (0 / -inf) past
+// the node's first / last label.  SBP_HSMEM: every lane stores its h into a
+// per-node shared-memory row [pad | h(Ms) | pad] and reads its taps back with
+// 128-bit loads (2 * ceil(R/4) LDS.128 instead of 2R shuffles + selects),
+// for R >= 5.
+// Blocks are 4 warps (every kernel that calls band_message launches 128
+// threads); the row of a node is private to its warp.
+template <int DOM, int VL, int LP, int R>
+struct BandTaps {
+    static constexpr int RL = (R + 3) / 4 * 4;   // floats fetched per side
+    float lo[RL], hi[RL];
+
+    __device__ __forceinline__ void fetch(const float (&h)[VL], int j, int x0) {
+        // narrow bands keep the shuffles (fewer instructions at R <= 4 in SASS)
+        if constexpr (SBP_HSMEM && R >= 5) {
+        constexpr int PPW = 32 / LP, MS = VL * LP, PADF = RL < 4 ? 4 : RL;
+        constexpr int ROW = MS + 2 * PADF;
+        constexpr float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+        __shared__ __align__(16) float hsm[4 * PPW * ROW];
+        float *row = hsm + ((threadIdx.x >> 5) * PPW + (threadIdx.x & 31) / LP) * ROW;
+        __syncwarp();   // the previous message's reads of this row are done
+#pragma unroll
+        for (int i = 0; i < VL; i += 4)
+            *reinterpret_cast<float4 *>(row + PADF + x0 + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+        if (j == 0) {
+#pragma unroll
+            for (int i = 0; i < PADF; i += 4) *reinterpret_cast<float4 *>(row + i) = make_float4(PAD, PAD, PAD, PAD);
+        }
+        if (j == LP - 1) {
+#pragma unroll
+            for (int i = 0; i < PADF; i += 4)
+                *reinterpret_cast<float4 *>(row + PADF + MS + i) = make_float4(PAD, PAD, PAD, PAD);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < RL; i += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(row + PADF + x0 - RL + i);
+            lo[i] = v.x; lo[i + 1] = v.y; lo[i + 2] = v.z; lo[i + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < RL; i += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(row + PADF + x0 + VL + i);
+            hi[i] = v.x; hi[i + 1] = v.y; hi[i + 2] = v.z; hi[i + 3] = v.w;
+        }
+        } else {
+#pragma unroll
+        for (int t = -R; t < 0; ++t) lo[RL + t] = band_h<DOM, VL, LP, R>(h, t, j);
+#pragma unroll
+        for (int t = VL; t < VL + R; ++t) hi[t - VL] = band_h<DOM, VL, LP, R>(h, t, j);
+        }
+    }
+
+    __device__ __forceinline__ float at(const float (&h)[VL], int t) const {
+        return t < 0 ? lo[RL + t] : (t < VL ? h[t] : hi[t - VL]);
+    }
+};
 
 // Three-input max (sm_100 FMNMX3): exact, same NaN rule as fmaxf.
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -244,23 +302,12 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
     // Label pairs (out[i], out[i+1]) take the weights (w(d), w(d-1)) of the
     // pair table in one packed op; taps outside |d| <= R carry the pad weight
     // (0 / -inf), exact no-ops, so every pair op is unconditional.
+    BandTaps<DOM, VL, LP, R> taps;
+    taps.fetch(h, j, x0);
     if (DOM == SBP_SUM) {
-#if SBP_BAND_FORM == 1
-        // d outer (ascending d is ascending x_i for every output), label pairs
-        // inner: one FFMA2 per pair and tap with the weight as a broadcast
-        // scalar, so the weights stay uniform operands
-        float hx[VL + 2 * R];
-#pragma unroll
-        for (int t = -R; t < VL + R; ++t) hx[t + R] = band_h<DOM, VL, LP, R>(h, t, j);
-#pragma unroll
-        for (int d = -R; d <= R; ++d)
-#pragma unroll
-            for (int i = 0; i < VL; i += 2)
-                fma2b(out[i], out[i + 1], hx[i + d + R], hx[i + d + R + 1], a.w[O][d + R]);
-#else
 #pragma unroll
         for (int t = -R; t < VL + R; ++t) {
-            const float hv = band_h<DOM, VL, LP, R>(h, t, j);
+            const float hv = taps.at(h, t);
 #pragma unroll
             for (int i = 0; i < VL; i += 2) {
                 const int d = t - i;
@@ -268,14 +315,13 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
                 fma2(out[i], out[i + 1], a.wp[O][d + R + 1], hv);
             }
         }
-#endif
     } else {
         // two taps per FMNMX3 (the max is exact: any grouping gives the same bits)
 #pragma unroll
         for (int t = -R; t < VL + R; t += 2) {
             const bool has1 = t + 1 < VL + R;
-            const float hv0 = band_h<DOM, VL, LP, R>(h, t, j);
-            const float hv1 = has1 ? band_h<DOM, VL, LP, R>(h, t + 1, j) : 0.0f;
+            const float hv0 = taps.at(h, t);
+            const float hv1 = has1 ? taps.at(h, t + 1) : 0.0f;
 #pragma unroll
             for (int i = 0; i < VL; i += 2) {
                 const int d0 = t - i, d1 = t + 1 - i;
