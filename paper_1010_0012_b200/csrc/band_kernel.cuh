@@ -25,7 +25,7 @@
 #include "sbp_common.cuh"
 
 #ifndef SBP_HSMEM
-#define SBP_HSMEM 1   // out-of-lane band taps through shared memory (0: shuffles)
+#define SBP_HSMEM 0   // 1: out-of-lane band taps through shared memory (measured slower, profiles/r01_ab_hsmem.txt)
 #endif
 
 namespace sbp {
