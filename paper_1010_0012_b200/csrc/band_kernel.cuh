@@ -230,6 +230,17 @@ __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const fl
     if (VL % 2 == 1) h[VL - 1] = (s[VL - 1] - c) + (isfinite(s[VL - 1]) ? e[VL - 1] : 0.0f);
 }
 
+// Sum of a lane's VL labels: even and odd labels accumulate in the two halves
+// of a packed pair (FADD2), then combine -- half the instructions and half
+// the dependent-add chain of a serial sum.
+template <int VL>
+__device__ __forceinline__ float vsum(const float (&v)[VL]) {
+    float s0 = v[0], s1 = v[1];
+#pragma unroll
+    for (int i = 2; i < VL; i += 2) add2(s0, s1, s0, s1, v[i], v[i + 1]);
+    return s0 + s1;
+}
+
 // Pairwise helpers over VL-label arrays (VL even).
 template <int VL>
 __device__ __forceinline__ void vmul(float (&r)[VL], const float (&a)[VL], const float (&b)[VL]) {
@@ -282,10 +293,7 @@ template <int DOM, int VL, int LP, int R, int O>
 __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)[VL], int j,
                                              int x0, float (&out)[VL]) {
     if (DOM == SBP_SUM) {
-        float s = 0.0f;
-#pragma unroll
-        for (int i = 0; i < VL; ++i) s += h[i];
-        s = lanes_sum<LP>(s);
+        const float s = lanes_sum<LP>(vsum(h));
         const float base = a.floor_term ? a.fbar[O] * s : 0.0f;
 #pragma unroll
         for (int i = 0; i < VL; ++i) out[i] = base;
@@ -351,10 +359,7 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
             for (int i = 0; i < VL; ++i)
                 if (x0 + i >= a.M) out[i] = 0.0f;
         }
-        float s = 0.0f;
-#pragma unroll
-        for (int i = 0; i < VL; ++i) s += out[i];
-        s = lanes_sum<LP>(s);
+        const float s = lanes_sum<LP>(vsum(out));
         ok = (s > 0.0f) && !isinf(s);
         const float inv = __frcp_rn(s);
 #pragma unroll
