@@ -214,15 +214,22 @@ __global__ void __launch_bounds__(DTHREADS, 1) dense_iter_kernel(const __grid_co
                             for (int i = 0; i < S::PT; ++i) hv[u][i] = hrow[i];
                         }
                     }
+                    // label pairs in packed FP32 (FFMA2 / FADD2): same roundings
 #pragma unroll
                     for (int i = 0; i < S::PT; ++i)
 #pragma unroll
-                        for (int l = 0; l < 8; ++l) {
-                            if (DOM == SBP_SUM)
-                                acc[i][l] = fmaf(bv[0][l], hv[0][i], acc[i][l]);
-                            else
-                                acc[i][l] = fmax3(acc[i][l], bv[0][l] + hv[0][i],
-                                                  bv[KS - 1][l] + hv[KS - 1][i]);
+                        for (int l = 0; l < 8; l += 2) {
+                            if (DOM == SBP_SUM) {
+                                fma2(acc[i][l], acc[i][l + 1], make_float2(bv[0][l], bv[0][l + 1]),
+                                     hv[0][i]);
+                            } else {
+                                float a0, a1, b0, b1;
+                                add2(a0, a1, bv[0][l], bv[0][l + 1], hv[0][i], hv[0][i]);
+                                add2(b0, b1, bv[KS - 1][l], bv[KS - 1][l + 1], hv[KS - 1][i],
+                                     hv[KS - 1][i]);
+                                acc[i][l] = fmax3(acc[i][l], a0, b0);
+                                acc[i][l + 1] = fmax3(acc[i][l + 1], a1, b1);
+                            }
                         }
                 }
                 __syncthreads();
