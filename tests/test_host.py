@@ -207,7 +207,7 @@ def test_oracle_sync_matches_per_edge_composition():
                 np.testing.assert_array_equal(out[ws, dst], res * (1.0 / s))
 
 
-def _plan_name(cfg_name, domain, sequential=False):
+def _band_structs(cfg_name, domain):
     cfg = synth.CONFIGS[cfg_name]
     Ms = L.lib().sbp_padded_labels(cfg.M)
     pl = plan.plan_potential(cfg.build_potential(), domain, "fast", cfg.M, Ms)
@@ -216,10 +216,56 @@ def _plan_name(cfg_name, domain, sequential=False):
         dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
     s = engine.GridEngine._make_pot_struct(_E(), pl)
     g = L.SbpGrid(cfg.height, cfg.width, cfg.M, Ms, 0, cfg.height)
+    return g, s, pl
+
+
+def _plan_name(cfg_name, domain, sequential=False):
+    g, s, _ = _band_structs(cfg_name, domain)
     buf = ctypes.create_string_buffer(128)
-    L.check(L.lib().sbp_plan_name(ctypes.byref(g), ctypes.byref(s), 1 if sequential else 0,
-                                  buf, 128))
+    mode = {False: 0, True: 1}.get(sequential, sequential)
+    L.check(L.lib().sbp_plan_name(ctypes.byref(g), ctypes.byref(s), mode, buf, 128))
     return buf.value.decode()
+
+
+def test_fused_plan_names():
+    # mode 2 = sbp_iterate_fused; label sets below 32 have no fused kernel and
+    # report the one-iteration kernel
+    assert _plan_name("C4", "sum", 2) == "band_fused_kernel<sum,VL=16,LP=8,R=7,rolled>"
+    assert _plan_name("C3", "max", 2) == "band_fused_kernel<max,VL=8,LP=8,R=3>"
+    assert _plan_name("C5_T2", "sum", 2) == "band_fused_kernel<sum,VL=16,LP=16,R=1>"
+    assert _plan_name("C1", "sum", 2) == _plan_name("C1", "sum", 0)
+
+
+def test_iterate_fused_validates_without_touching_the_device():
+    g, s, _ = _band_structs("C4", "sum")
+    lib = L.lib()
+    words = lib.sbp_fused_stamp_words(ctypes.byref(g))
+    assert words == 4 * g.rows * g.W
+    p = ctypes.c_void_p(0x1000)   # never dereferenced: validation fails first
+
+    def call(levels=2, epoch=1, lag=4, rounds=2, ptr=p, pot=s):
+        return lib.sbp_iterate_fused(ctypes.byref(g), ctypes.byref(pot), ptr, ptr, ptr, levels,
+                                     0, 0, ptr, epoch, lag, rounds, ptr, None)
+    assert call(levels=0) == L.SBP_EINVAL
+    assert call(levels=5) == L.SBP_EINVAL
+    assert call(lag=1) == L.SBP_EINVAL
+    assert call(rounds=0) == L.SBP_EINVAL
+    assert call(epoch=0) == L.SBP_EINVAL
+    assert call(ptr=None) == L.SBP_EINVAL
+    ell = L.SbpPotential()
+    ell.kind, ell.domain = L.SBP_POT_ELL, L.SBP_SUM
+    assert call(pot=ell) == L.SBP_EUNSUPPORTED
+
+
+def test_default_fusion_policy(monkeypatch):
+    monkeypatch.delenv("SBP_FUSE", raising=False)
+    for name, domain, want in [("C5_T2", "sum", 3), ("C5_T2", "max", 1), ("C4", "sum", 1),
+                               ("C5_T9", "sum", 1)]:
+        g, _, pl = _band_structs(name, domain)
+        assert engine._default_fuse(domain, g.Ms, pl) == want, name
+    monkeypatch.setenv("SBP_FUSE", "2")
+    g, _, pl = _band_structs("C4", "sum")
+    assert engine._default_fuse("sum", g.Ms, pl) == 2
 
 
 @pytest.mark.parametrize("name,domain,expect", [
