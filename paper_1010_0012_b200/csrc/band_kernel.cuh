@@ -390,8 +390,11 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const IterCtx 
     const bool ok = band_message<DOM, VL, LP, R, O>(a, h, j, x0, out);
     if (!active) return;
     const long long W = a.W;
+    // node part (loop-invariant in the rolled kernel) + a warp-uniform
+    // direction offset: slot of the neighbour and the step to it
     const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
-    float *dst = it.msgs_out + dir_wslot(DIR) * a.slot_stride + (node_l + step) * a.Ms + x0;
+    const long long dir_off = dir_wslot(DIR) * a.slot_stride + step * a.Ms;
+    float *dst = it.msgs_out + (node_l * a.Ms + x0) + dir_off;
     Vec8Loader<VL>::store(dst, out);
     if (!ok && j == 0) report_failure(a.err, it.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
