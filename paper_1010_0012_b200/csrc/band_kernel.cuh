@@ -783,8 +783,11 @@ cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
 // ... (T = resident warps).  (An L2 prefetch of the next group measured
 // slower on C4 and was dropped; the TMA-staged variant below is the
 // latency-hiding version.)
+#ifndef SBP_VL16_BLOCKS
+#define SBP_VL16_BLOCKS 4   // resident 128-thread blocks per SM asked of ptxas for VL = 16, R <= 8
+#endif
 template <int DOM, int VL, int LP, int R, bool ROLLED>
-__global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : (R <= 8 ? 4 : 3)))
+__global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : (R <= 8 ? SBP_VL16_BLOCKS : 3)))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
     const IterCtx it = iter_of(a);

@@ -1,7 +1,7 @@
 # current build (libsbp.so) vs the previous one (libsbp_prev.so): cold + sustained
 out=gpurun_out/ab_prev.txt
 rm -f $out
-LIBS="libsbp.so libsbp_prev.so"
+LIBS="libsbp.so ${ALT_LIB:-libsbp_prev.so}"
 for c in C4:sum C3:max C5_T9:sum C5_T17:sum C5_T33:sum C2:sum; do
   n=${c%%:*}; d=${c##*:}
   for l in $LIBS; do
