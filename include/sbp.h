@@ -140,7 +140,7 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
  * afterwards.  Bit-identical to `levels` sbp_iterate calls.  stamps: device
  * array of sbp_fused_stamp_words(g) uint32, zero-filled once; epoch: a
  * non-zero value never used before with this stamps array.  Band potentials,
- * Ms >= 32, R <= 16; otherwise SBP_EUNSUPPORTED. */
+ * Ms >= 32, compiled radius R in {1..4, 7, 8}; otherwise SBP_EUNSUPPORTED. */
 SBP_API int sbp_fused_stamp_words(const sbp_grid *g);
 SBP_API int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *values,
                               float *msgs_a, float *msgs_b, int levels, int iteration,

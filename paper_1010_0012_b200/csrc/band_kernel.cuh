@@ -832,7 +832,7 @@ cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
 
 // Band radii with a compiled kernel; a potential of radius r runs on the
 // smallest listed R >= r (extra taps carry weight 0 / -inf: exact no-ops).
-#define SBP_BAND_RADII(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
+#define SBP_BAND_RADII(X) X(1) X(2) X(3) X(4) X(7) X(8) X(16) X(32)
 
 template <int MS, int DOM, int VL, bool ROLLED>
 BandLaunchFn pick_band_r(int R) {

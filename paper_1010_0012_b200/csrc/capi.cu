@@ -75,7 +75,7 @@ int check_grid(const sbp_grid *g) {
     return SBP_OK;
 }
 
-const int kRadii[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32};
+const int kRadii[] = {1, 2, 3, 4, 7, 8, 16, 32};   // = SBP_BAND_RADII (band_kernel.cuh)
 
 // Band kernel variant choice, from the B200 A/B runs (tools/ab_vl.sh,
 // tools/ab_staged.sh; profiles/r01_kernel_variants.md).  Environment

@@ -192,7 +192,8 @@ cudaError_t launch_band_fused(const BandArgs &a, FusedArgs &f, cudaStream_t s) {
                                        dim3((unsigned)blocks), dim3(128), args, 0, s);
 }
 
-// Fused kernels exist for the register-loaded variants at R <= 16, with the
+// Fused kernels exist for the register-loaded variants at R in {1..4, 7, 8}
+// (the BASELINE bands up to m = 17; wider bands measured slower fused), with the
 // lane width the one-iteration kernel uses (VL = 16 for sum, Ms >= 128,
 // R <= 8; else 8); `rolled` (symmetric potentials) for R in {4, 7, 8}.
 // Ms >= 32 only: a node's slot vector must cover whole 128-byte L2 lines for
@@ -205,7 +206,7 @@ FusedLaunchFn pick_fused(int R, bool rolled) {
         switch (R) {
 #define SBP_CASE(RR)                                                                  \
     case RR:                                                                          \
-        if constexpr (RR < MS && RR <= 16) {                                          \
+        if constexpr (RR < MS && (RR <= 4 || RR == 7 || RR == 8)) {                   \
             constexpr int VLF = (DOM == SBP_SUM && MS >= 128 && RR <= 8) ? 16 : 8;    \
             if constexpr (RR == 4 || RR == 7 || RR == 8)                              \
                 if (rolled) return &launch_band_fused<DOM, VLF, MS / VLF, RR, true>;  \
