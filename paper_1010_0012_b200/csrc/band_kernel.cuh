@@ -24,6 +24,15 @@
 
 #include "sbp_common.cuh"
 
+#ifndef SBP_L1NA
+#define SBP_L1NA 0   // 1: streaming loads / stores skip L1 allocation
+#endif
+#if SBP_L1NA
+#define SBP_L1_HINT ".L1::no_allocate"
+#else
+#define SBP_L1_HINT ""
+#endif
+
 #ifndef SBP_HSMEM
 #define SBP_HSMEM 0   // 1: out-of-lane band taps through shared memory (measured slower, profiles/r01_ab_hsmem.txt)
 #endif
@@ -77,7 +86,7 @@ struct Vec8Loader {
         for (int c = 0; c < N / 8; ++c) {
             const float *p = src + 8 * c;
             asm volatile(
-                "ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                "ld.global.nc" SBP_L1_HINT ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                 : "=f"(dst[8 * c + 0]), "=f"(dst[8 * c + 1]), "=f"(dst[8 * c + 2]),
                   "=f"(dst[8 * c + 3]), "=f"(dst[8 * c + 4]), "=f"(dst[8 * c + 5]),
                   "=f"(dst[8 * c + 6]), "=f"(dst[8 * c + 7])
@@ -88,7 +97,7 @@ struct Vec8Loader {
 #pragma unroll
         for (int c = 0; c < N / 8; ++c) {
             float *p = dst + 8 * c;
-            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+            asm volatile("st.global" SBP_L1_HINT ".v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                          "f"(v[8 * c + 0]), "f"(v[8 * c + 1]), "f"(v[8 * c + 2]),
                          "f"(v[8 * c + 3]), "f"(v[8 * c + 4]), "f"(v[8 * c + 5]),
                          "f"(v[8 * c + 6]), "f"(v[8 * c + 7])

@@ -8,8 +8,9 @@
 // the incoming slot `wslot` of src+step, which the next step of the same chain
 // reads.  Chains only read slots no other chain of the pass writes, so they
 // run in parallel: LP lanes per chain, the chained message carried in
-// registers, the next node's unary and two other incoming vectors loaded one
-// step ahead and L2-prefetched CHAIN_PF steps ahead.  The per-message
+// registers, the next CHAIN_LA nodes' unary and two other incoming vectors
+// in a register ring (loaded CHAIN_LA steps ahead), L2-prefetched CHAIN_PF
+// steps ahead.  The per-message
 // arithmetic is band_message() of the synchronous kernel: same products in
 // the reference order, same error-free max-sum h, same normalisation.
 #pragma once
@@ -18,7 +19,12 @@
 
 namespace sbp {
 
-constexpr int CHAIN_PF = 4;   // L2 prefetch distance (steps)
+// register lookahead (steps): 3 for sum-product (C4 5.11 vs 6.33 ms per
+// sweep, C5 T=9 2.93 vs 3.65; profiles/r01_ab_seq.txt); max-sum keeps one
+// step (its TwoSum state leaves no registers: 3 steps measured 4 % slower)
+template <int DOM>
+constexpr int chain_lookahead() { return DOM == SBP_SUM ? 3 : 1; }
+constexpr int CHAIN_PF = 12;   // L2 prefetch distance (steps)
 
 // Geometry of pass `dir` (numba_kernels.py:230-245 `_grid_step`).
 struct PassGeom {
@@ -60,6 +66,7 @@ __device__ __forceinline__ void chain_h(const float (&g)[VL], const float (&ma)[
 template <int DOM, int VL, int LP, int R>
 __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__ BandArgs a) {
     constexpr int CPW = 32 / LP;   // chains per warp
+    constexpr int CHAIN_LA = chain_lookahead<DOM>();
     const int dir = a.pass;
     const PassGeom geo = pass_geom(dir, a.H, a.W);
     const int lane = threadIdx.x & 31;
@@ -79,54 +86,61 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__
     const int sb = (dir <= 1) ? 3 : 2;
     auto node_ptr = [&](int slot, long long n) { return msgs + slot * S + (n + W) * a.Ms + x0; };
 
-    float chain[VL], g[VL], m_a[VL], m_b[VL];
+    // the chained message lives in registers; the next CHAIN_LA nodes' unary
+    // and two other incoming vectors (independent of the chain) sit in a
+    // register ring, loaded CHAIN_LA steps ahead; L2 prefetch CHAIN_PF ahead
+    float chain[VL], gq[CHAIN_LA][VL], aq[CHAIN_LA][VL], bq[CHAIN_LA][VL];
     Vec8Loader<VL>::load(chain, node_ptr(geo.wslot, src0));
-    Vec8Loader<VL>::load(g, a.values + src0 * a.Ms + x0);
-    Vec8Loader<VL>::load(m_a, node_ptr(sa, src0));
-    Vec8Loader<VL>::load(m_b, node_ptr(sb, src0));
-
-    for (long long pos = 0; pos < geo.line_len; ++pos) {
-        const long long src = src0 + pos * geo.step;
-        // next node's inputs (independent of the chain): load one step ahead,
-        // prefetch CHAIN_PF steps ahead into L2
-        float gn[VL], ma_n[VL], mb_n[VL];
-        const bool more = pos + 1 < geo.line_len;
-        if (more) {
-            const long long nx = src + geo.step;
-            Vec8Loader<VL>::load(gn, a.values + nx * a.Ms + x0);
-            Vec8Loader<VL>::load(ma_n, node_ptr(sa, nx));
-            Vec8Loader<VL>::load(mb_n, node_ptr(sb, nx));
-            if (j == 0 && pos + CHAIN_PF < geo.line_len) {
+    const long long len = geo.line_len;
+#pragma unroll
+    for (int k = 0; k < CHAIN_LA; ++k) {
+        if (k < len) {
+            const long long n = src0 + k * geo.step;
+            Vec8Loader<VL>::load(gq[k], a.values + n * a.Ms + x0);
+            Vec8Loader<VL>::load(aq[k], node_ptr(sa, n));
+            Vec8Loader<VL>::load(bq[k], node_ptr(sb, n));
+        }
+    }
+    for (long long base = 0; base < len; base += CHAIN_LA) {
+#pragma unroll
+        for (int k = 0; k < CHAIN_LA; ++k) {
+            const long long pos = base + k;
+            if (pos >= len) break;   // warp-uniform: the chains of a warp have one length
+            const long long src = src0 + pos * geo.step;
+            if (j == 0 && pos + CHAIN_PF < len) {
                 const long long pf = src + CHAIN_PF * geo.step;
                 const unsigned bytes = (unsigned)(a.Ms * 4);
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.values + pf * a.Ms), "r"(bytes) : "memory");
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(msgs + sa * S + (pf + W) * a.Ms), "r"(bytes) : "memory");
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(msgs + sb * S + (pf + W) * a.Ms), "r"(bytes) : "memory");
             }
-        }
-        // included slots in ascending order for each pass:
-        //   0 (excl 2, chain 1): m0 m1 m3 = a, chain, b
-        //   1 (excl 1, chain 2): m0 m2 m3 = a, chain, b
-        //   2 (excl 3, chain 0): m0 m1 m2 = chain, a, b
-        //   3 (excl 0, chain 3): m1 m2 m3 = a, b, chain
-        float h[VL];
-        if (dir <= 1) chain_h<DOM, VL, LP>(g, m_a, chain, m_b, dir, h);
-        else if (dir == 2) chain_h<DOM, VL, LP>(g, chain, m_a, m_b, dir, h);
-        else chain_h<DOM, VL, LP>(g, m_a, m_b, chain, dir, h);
-        bool ok;
-        if (dir == 0 || dir == 2) ok = band_message<DOM, VL, LP, R, 0>(a, h, j, x0, chain);
-        else ok = band_message<DOM, VL, LP, R, 1>(a, h, j, x0, chain);
-        if (valid) Vec8Loader<VL>::store(node_ptr(geo.wslot, src + geo.step), chain);
-        if (!ok && valid && j == 0) {
-            // reference order of the first failure: sweep, pass, line, position
-            const unsigned long long key = ((unsigned long long)a.iteration << 40) |
-                                           ((unsigned long long)dir << 38) |
-                                           (unsigned long long)(line * geo.line_len + pos);
-            atomicMin(a.err, key);
-        }
-        if (more) {
-#pragma unroll
-            for (int i = 0; i < VL; ++i) { g[i] = gn[i]; m_a[i] = ma_n[i]; m_b[i] = mb_n[i]; }
+            // included slots in ascending order for each pass:
+            //   0 (excl 2, chain 1): m0 m1 m3 = a, chain, b
+            //   1 (excl 1, chain 2): m0 m2 m3 = a, chain, b
+            //   2 (excl 3, chain 0): m0 m1 m2 = chain, a, b
+            //   3 (excl 0, chain 3): m1 m2 m3 = a, b, chain
+            float h[VL];
+            if (dir <= 1) chain_h<DOM, VL, LP>(gq[k], aq[k], chain, bq[k], dir, h);
+            else if (dir == 2) chain_h<DOM, VL, LP>(gq[k], chain, aq[k], bq[k], dir, h);
+            else chain_h<DOM, VL, LP>(gq[k], aq[k], bq[k], chain, dir, h);
+            // refill this ring slot with the node CHAIN_LA steps ahead
+            if (pos + CHAIN_LA < len) {
+                const long long n = src + CHAIN_LA * geo.step;
+                Vec8Loader<VL>::load(gq[k], a.values + n * a.Ms + x0);
+                Vec8Loader<VL>::load(aq[k], node_ptr(sa, n));
+                Vec8Loader<VL>::load(bq[k], node_ptr(sb, n));
+            }
+            bool ok;
+            if (dir == 0 || dir == 2) ok = band_message<DOM, VL, LP, R, 0>(a, h, j, x0, chain);
+            else ok = band_message<DOM, VL, LP, R, 1>(a, h, j, x0, chain);
+            if (valid) Vec8Loader<VL>::store(node_ptr(geo.wslot, src + geo.step), chain);
+            if (!ok && valid && j == 0) {
+                // reference order of the first failure: sweep, pass, line, position
+                const unsigned long long key = ((unsigned long long)a.iteration << 40) |
+                                               ((unsigned long long)dir << 38) |
+                                               (unsigned long long)(line * len + pos);
+                atomicMin(a.err, key);
+            }
         }
     }
 }
