@@ -20,7 +20,7 @@ BandLaunchFn pick_band(int dom, int vl, int R, int rolled) {
 
 namespace sbp {
 template <int MS, int DOM>
-BandLaunchFn pick_chain(int R);
+BandLaunchFn pick_chain(int R, int vl);
 // instantiated in band_ms*_*.cu (keeps this file from compiling every kernel)
 #define SBP_EXTERN(MSV)                                                          \
     extern template BandLaunchFn pick_band_dom<MSV, SBP_SUM>(int, int, int);      \
@@ -410,11 +410,13 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
     for (int r : kRadii)
         if (r >= pot->R && r < g->Ms) { Rk = r; break; }
     sbp::BandLaunchFn fn = nullptr;
+    // chain lane width: SBP_CHAIN_VL=16 (sum, Ms >= 128, R <= 8) or 8
+    const int chain_vl = env_int("SBP_CHAIN_VL", 8);
     if (Rk) {
 #define SBP_C(MSV)                                                                          \
     case MSV:                                                                               \
-        fn = pot->domain == SBP_SUM ? sbp::pick_chain<MSV, SBP_SUM>(Rk)                     \
-                                    : sbp::pick_chain<MSV, SBP_MAX>(Rk);                    \
+        fn = pot->domain == SBP_SUM ? sbp::pick_chain<MSV, SBP_SUM>(Rk, chain_vl)           \
+                                    : sbp::pick_chain<MSV, SBP_MAX>(Rk, chain_vl);          \
         break;
         switch (g->Ms) { SBP_C(8) SBP_C(16) SBP_C(32) SBP_C(64) SBP_C(128) SBP_C(256) default: break; }
 #undef SBP_C
@@ -450,7 +452,9 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         for (int r : kRadii)
             if (r >= pot->R && r < g->Ms) { Rk = r; break; }
         if (sequential == 1) {
-            snprintf(buf, len, "chain_pass_kernel<%s,VL=8,LP=%d,R=%d>", dom, g->Ms / 8, Rk);
+            const int cvl = (env_int("SBP_CHAIN_VL", 8) == 16 && pot->domain == SBP_SUM &&
+                             g->Ms >= 128 && Rk <= 8) ? 16 : 8;
+            snprintf(buf, len, "chain_pass_kernel<%s,VL=%d,LP=%d,R=%d>", dom, cvl, g->Ms / cvl, Rk);
         } else if (sequential == 2 && Rk && fused_fn(g->Ms, pot->domain, Rk, false)) {
             const int vl = (pot->domain == SBP_SUM && g->Ms >= 128 && Rk <= 8) ? 16 : 8;
             snprintf(buf, len, "band_fused_kernel<%s,VL=%d,LP=%d,R=%d%s>", dom, vl, g->Ms / vl, Rk,

@@ -22,8 +22,8 @@ namespace sbp {
 // register lookahead (steps): 3 for sum-product (C4 5.11 vs 6.33 ms per
 // sweep, C5 T=9 2.93 vs 3.65; profiles/r01_ab_seq.txt); max-sum keeps one
 // step (its TwoSum state leaves no registers: 3 steps measured 4 % slower)
-template <int DOM>
-constexpr int chain_lookahead() { return DOM == SBP_SUM ? 3 : 1; }
+template <int DOM, int VL>
+constexpr int chain_lookahead() { return DOM == SBP_SUM ? (VL == 8 ? 3 : 1) : 1; }
 constexpr int CHAIN_PF = 12;   // L2 prefetch distance (steps)
 
 // Geometry of pass `dir` (numba_kernels.py:230-245 `_grid_step`).
@@ -66,7 +66,7 @@ __device__ __forceinline__ void chain_h(const float (&g)[VL], const float (&ma)[
 template <int DOM, int VL, int LP, int R>
 __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__ BandArgs a) {
     constexpr int CPW = 32 / LP;   // chains per warp
-    constexpr int CHAIN_LA = chain_lookahead<DOM>();
+    constexpr int CHAIN_LA = chain_lookahead<DOM, VL>();
     const int dir = a.pass;
     const PassGeom geo = pass_geom(dir, a.H, a.W);
     const int lane = threadIdx.x & 31;
@@ -163,12 +163,16 @@ cudaError_t launch_chain(const BandArgs &a, cudaStream_t s) {
 }
 
 template <int MS, int DOM>
-BandLaunchFn pick_chain(int R) {
+BandLaunchFn pick_chain(int R, int vl) {
     switch (R) {
 #define SBP_CASE(RR)                                                         \
     case RR:                                                                 \
-        if constexpr (RR < MS) return &launch_chain<DOM, 8, MS / 8, RR>;     \
-        else return nullptr;
+        if constexpr (RR < MS) {                                             \
+            if constexpr (DOM == SBP_SUM && MS >= 128 && RR <= 8)            \
+                if (vl == 16) return &launch_chain<DOM, 16, MS / 16, RR>;    \
+            return &launch_chain<DOM, 8, MS / 8, RR>;                        \
+        }                                                                    \
+        return nullptr;
         SBP_BAND_RADII(SBP_CASE)
 #undef SBP_CASE
     default: return nullptr;
