@@ -343,7 +343,7 @@ def run_ours(args, cfg):
         "metric": "directed_message_updates_per_s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded random-dot stereo, 8-rectangle disparity, sigma=5 noise)",
+        "data": f"synthetic (seeded random-dot stereo, 8-rectangle disparity, sigma={cfg.sigma:g} noise)",
         "config": config_dict(cfg, args, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak,
