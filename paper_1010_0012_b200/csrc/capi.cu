@@ -100,7 +100,11 @@ BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
     // packed-FP32 build, B200 A/B (profiles/r01_ab_packed.txt): the rolled
     // VL=16 kernel is the fastest for C4 (sum, Ms=128, R=7) cold and
     // sustained; rolled instantiations exist for R in {4, 7, 8} and R >= 24
-    const bool rolled_c4 = sym && domain == SBP_SUM && Ms == 128 && (Rk == 4 || Rk == 7 || Rk == 8);
+    // (and for C5 T=9, sum, Ms=256, R=8: 1.51 vs 1.69 ms, r01_ab_rolled_more.txt;
+    // at Ms=256 R=4 the staged kernel stays faster, max-sum never rolls)
+    const bool rolled_c4 = sym && domain == SBP_SUM &&
+                           ((Ms == 128 && (Rk == 4 || Rk == 7 || Rk == 8)) ||
+                            (Ms == 256 && (Rk == 7 || Rk == 8)));
     if ((sym && Rk >= band_roll_min_r()) || (rolled_c4 && env_int("SBP_ROLL_MIN_R", 0) != 99)) {
         c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
         c.variant = 1;

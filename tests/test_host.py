@@ -273,7 +273,7 @@ def test_default_fusion_policy(monkeypatch):
     ("C3", "max", "band_iter_staged_kernel<max,VL=8,LP=8,R=3>"),
     ("C2", "sum", "band_iter_kernel<sum,VL=8,LP=4,R=2>"),
     ("C5_T5", "sum", "band_iter_staged_kernel<sum,VL=16,LP=16,R=4>"),
-    ("C5_T9", "sum", "band_iter_kernel<sum,VL=16,LP=16,R=8>"),
+    ("C5_T9", "sum", "band_iter_kernel<sum,VL=16,LP=16,R=8,rolled>"),
     ("C5_T17", "sum", "band_iter_staged_kernel<sum,VL=8,LP=32,R=16>"),
 ])
 def test_default_kernel_choice(name, domain, expect):

@@ -3,7 +3,10 @@
 #  2. C4 sustained (bench --kernel-only) and cold (kbench) per build/variant
 #  3. other configs, cold, default variant per build
 # Builds: libsbp.so (packed, label-pair x weight-pair form), libsbp_f1.so
-# (packed, broadcast-weight form), libsbp_scalar.so (scalar FP32 ops).
+# (packed, broadcast-weight form; that form has since been removed, so this
+# script is the record of the round-1 run, profiles/r01_ab_packed.txt),
+# libsbp_scalar.so (scalar FP32 ops):
+#   make -C paper_1010_0012_b200/csrc BUILD=_build_scalar EXTRA=-DSBP_SCALAR_F32 LIB=../libsbp_scalar.so
 out=gpurun_out/ab_packed.txt
 rm -f $out
 LIBS="libsbp.so libsbp_f1.so libsbp_scalar.so"
