@@ -31,8 +31,21 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TF/s (no measured FP32 peak)
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 TF/s at the max SM clock
 FALLBACK_HBM_GBS = 6650.0                               # B200_PROFILING.md fallback
+
+
+def fp32_peak():
+    """FP32 ceiling (TFLOP/s): the measured FFMA rate and, for max-sum, the
+    measured FADD2 + FMNMX3 rate (one add and one max per band candidate,
+    tools/pipes.cu), from the committed microbenchmark record; else nominal."""
+    p = ROOT / "profiles" / "fp32_peaks.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"sum": float(d["ffma_tflops"]), "max": float(d["add_max_tops"]),
+                "source": f"measured ({p.name}: {d.get('how', '')})"}
+    return {"sum": FP32_NOMINAL_TFLOPS, "max": FP32_NOMINAL_TFLOPS,
+            "source": "nominal 148 SM x 128 lanes x 2 x 1.965 GHz"}
 
 
 def peaks():
@@ -182,6 +195,47 @@ def cpu_sample(cfg, domain: str, min_seconds: float = 10.0, max_iters: int = 3):
     return ups, cores, f"{its} synchronous iteration(s) of the full {H}x{W} M={M} grid, f64"
 
 
+def reference_run_sweeps_sample(cfg, domain: str, rows: int = 64, sweeps: int = 3):
+    """The as-shipped reference ``sparsebp.run_sweeps`` (its default: the
+    canonical in-place sequential schedule, numba, one thread by design,
+    SPEC.md:264) on a bounded sample -- the first ``rows`` rows of the same
+    seeded stereo pair -- timed on this host (BASELINE.md section 3 item 1,
+    reference bench.py:67-77: min over sweeps).  The reference is installed
+    unmodified under baseline/_ref (pip --target, git-ignored); returns None
+    if it is absent."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "sparsebp").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/sbp_numba_cache")
+    if str(ref_dir) not in sys.path:
+        sys.path.insert(0, str(ref_dir))
+    import sparsebp
+    from paper_1010_0012_b200 import synth
+    left, right, _ = synth.noisy_stereo_pair(cfg.height, cfg.width, cfg.M, cfg.sigma, 0)
+    params = sparsebp.StereoParams(M=cfg.M, alpha=cfg.alpha, T_b=cfg.T if cfg.potential == "linear"
+                                   else 2.0, beta=cfg.beta, T_u=cfg.T_u)
+    u, lu = sparsebp.stereo_unary_field(sparsebp.GrayImage(left[:rows]),
+                                        sparsebp.GrayImage(right[:rows]), params)
+    if cfg.potential == "linear":
+        pot = sparsebp.truncated_linear_potential(cfg.M, cfg.alpha, cfg.T)
+    else:
+        d = np.abs(np.arange(cfg.M)[:, None] - np.arange(cfg.M)[None, :]).astype(np.float64)
+        table = np.exp(-cfg.alpha * np.minimum(d * d, cfg.T))
+        pot = sparsebp.sparse_from_dense(table, fbar=table[0, -1])
+    model = sparsebp.build_grid_mrf(rows, cfg.width, cfg.M, u, pot, log_unary_provider=lu)
+    warm = sparsebp.build_grid_mrf(2, 3, cfg.M, u[:6], pot, log_unary_provider=lu[:6])
+    sparsebp.run_sweeps(warm, 1, kernel="fast", domain=domain)      # numba JIT / cache load
+    store = sparsebp.run_sweeps(model, sweeps, kernel="fast", domain=domain)
+    per_sweep = 2 * model.n_edges
+    best = min(store.stats.sweep_seconds)
+    return {"value": per_sweep / best, "unit": "updates/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"sparsebp.run_sweeps(kernel='fast', domain='{domain}') as shipped "
+                      f"(sequential schedule, numba, 1 thread) on rows 0..{rows - 1} of the "
+                      f"{cfg.height}x{cfg.width} M={cfg.M} grid; min of {sweeps} sweeps",
+            "sec_per_sweep": best}
+
+
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -221,6 +275,7 @@ def run_reference(args, cfg):
                          "sample": sample},
         "e2e": {"value": ups, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "as_shipped_run_sweeps": reference_run_sweeps_sample(cfg, args.domain),
     }
     print(json.dumps(line), flush=True)
 
@@ -329,12 +384,16 @@ def run_ours(args, cfg):
     # e2e through the public API with host buffers; CPU baseline at N=1 only
     e2e = None
     cpu = None
+    others = None
+    if world == 1 and not args.kernel_only and not args.no_configs:
+        others = configs_block(args, torch, dev)
     if not args.kernel_only:
         if world == 1:
             e2e = e2e_public_api(args, cfg, torch)
             ups, cores, sample = cpu_sample(cfg, args.domain)
             cpu = {"value": ups, "unit": "updates/s", "cores": cores, "kind": "port",
-                   "sample": sample}
+                   "sample": sample,
+                   "as_shipped_run_sweeps": reference_run_sweeps_sample(cfg, args.domain)}
         else:
             e2e = e2e_strips(args, cfg, torch, rank, world, dev)
     if rank != 0:
@@ -363,10 +422,81 @@ def run_ours(args, cfg):
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
+        "configs": others,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def configs_block(args, torch, dev):
+    """The other BASELINE configs, measured in the same run (driver-visible):
+    C3 (max-product, 100 iterations) and the C5 band-width sweep (M=256,
+    T in {2,5,9,17,33}, both domains, 20 iterations) with the banded kernel
+    against the dense O(M^2) comparison kernel on identical unaries.  Per
+    entry: median device ms per synchronous iteration (CUDA events on the
+    launching stream, steady state), directed updates/s, the roofline
+    max(B / HBM peak, F / FP32 peak) it is measured against, and the clocks
+    sampled while it ran."""
+    from paper_1010_0012_b200 import synth
+    from paper_1010_0012_b200.engine import GridEngine
+    hbm, _ = peaks()
+    fp = fp32_peak()
+    out = {"hbm_peak_gbs": hbm, "fp32_peak_tflops": {"sum": fp["sum"], "max": fp["max"]},
+           "fp32_peak_source": fp["source"], "entries": []}
+
+    def measure(eng, iters, cfg, domain, kernel):
+        eng.reset()
+        eng.step(2)
+        torch.cuda.synchronize()
+        evs: list = []
+        with ClockSampler(dev.index) as clk:
+            eng.step(iters, events=evs)
+            torch.cuda.synchronize()
+        eng.raise_if_degenerate()
+        per = sorted(a.elapsed_time(b) / k for a, b, k in evs)
+        ms = per[len(per) // 2]
+        pot = eng.model.shared_potential
+        B, F = algorithmic(cfg, pot)
+        if kernel == "standard":
+            F = cfg.n_directed * 2 * cfg.M * cfg.M
+        t_hbm = B / (hbm * 1e9) * 1e3
+        t_fp = F / (fp[domain] * 1e12) * 1e3
+        bound = "hbm" if t_hbm >= t_fp else "fp32"
+        return {"config": cfg.name, "domain": domain, "kernel": kernel,
+                "kernel_name": eng.kernel_name, "iterations": iters,
+                "ms_per_iteration": ms, "updates_per_s": cfg.n_directed / ms * 1e3,
+                "bytes_per_iteration": B, "flops_per_iteration": F,
+                "roofline": {"bound": bound, "ms": max(t_hbm, t_fp),
+                             "frac": max(t_hbm, t_fp) / ms, "hbm_frac": t_hbm / ms,
+                             "fp32_frac": t_fp / ms},
+                "clocks": clk.summary()}
+
+    cfg = synth.CONFIGS["C3"]
+    eng = GridEngine(synth.StripModel(cfg), "max", "fast", device=dev,
+                     values=synth.config_values(cfg, "max"))
+    out["entries"].append(measure(eng, cfg.iters, cfg, "max", "fast"))
+    del eng
+    torch.cuda.empty_cache()
+    for domain in ("sum", "max"):
+        vals = synth.config_values(synth.CONFIGS["C5_T2"], domain)
+        for T in (2, 5, 9, 17, 33):
+            cfg = synth.CONFIGS[f"C5_T{T}"]
+            band = None
+            for kernel in ("fast", "standard"):
+                eng = GridEngine(synth.StripModel(cfg), domain, kernel, device=dev, values=vals)
+                e = measure(eng, cfg.iters if kernel == "fast" else 6, cfg, domain, kernel)
+                if kernel == "fast":
+                    band = e
+                else:
+                    band["dense"] = {k: e[k] for k in ("kernel_name", "ms_per_iteration",
+                                                       "updates_per_s", "roofline")}
+                    band["speedup_band_over_dense"] = e["ms_per_iteration"] / band["ms_per_iteration"]
+                del eng
+                torch.cuda.empty_cache()
+            out["entries"].append(band)
+        del vals
+    return out
 
 
 def e2e_public_api(args, cfg, torch):
@@ -502,7 +632,9 @@ def main():
     ap.add_argument("--domain", default=None)
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--kernel-only", action="store_true",
-                    help="skip the e2e and CPU-baseline legs (kernel A/B runs)")
+                    help="skip the e2e, CPU-baseline and other-config legs (kernel A/B runs)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other-config block (C3, C5 band-width sweep)")
     args = ap.parse_args()
     from paper_1010_0012_b200 import synth
     cfg = synth.CONFIGS[args.config]

@@ -69,10 +69,16 @@ extern "C" {
 #define SBP_MAX_R 32
 #define SBP_ERR_NONE 0xffffffffffffffffull
 
+#define SBP_DEVICE_AUTO (-1)
+
 typedef struct {
     int H, W;      /* global grid */
     int M, Ms;     /* labels and padded per-node stride (multiple of 4) */
     int r0, rows;  /* this strip: global rows r0 .. r0+rows-1 */
+    int device;    /* CUDA device owning every buffer passed with this grid; the
+                      library (static CUDA runtime) selects it before launching.
+                      SBP_DEVICE_AUTO: look it up from the buffer pointers
+                      (cudaPointerGetAttributes on every call). */
 } sbp_grid;
 
 typedef struct {
@@ -98,13 +104,34 @@ typedef struct {
     const float *fbar_all;
     const int32_t *pid_h;
     const int32_t *pid_v;
+    /* Accumulation precision of sum-product (SBP_ACC_*): SBP_ACC_F64 computes
+     * products, sums and the normaliser in f64 from the f32-stored messages
+     * (reference precision, numba_kernels.py:44-54); ELL kind, shared potential
+     * only; the weights then carry f64 precision as ell_w (high f32 plane) +
+     * ell_w_lo (low plane) and fbar as fbar64. */
+    int accumulate;
+    double fbar64[2];
+    const float *ell_w_lo[2];
 } sbp_potential;
+
+#define SBP_ACC_F32 0
+#define SBP_ACC_F64 1
 
 SBP_API int sbp_version(void);
 SBP_API const char *sbp_last_error(void);
 
+/* The SBP_* environment knobs (kernel-variant overrides for A/B runs) are read
+ * once per process; this re-reads them. */
+SBP_API int sbp_reload_config(void);
+
 /* Padded label stride the band kernels use for M labels (>= M, multiple of 4). */
 SBP_API int sbp_padded_labels(int M);
+
+/* Compiled band radius a Toeplitz band of radius R runs on at padded stride
+ * Ms (the smallest compiled radius >= R that is < Ms), or 0 when no band
+ * kernel exists -- the host then plans the general ELL kernel instead
+ * (reference numba_kernels.py:44-54 runs any CSC; bp.py:466-489). */
+SBP_API int sbp_band_radius(int Ms, int R);
 
 /* Initial messages (bp.py:587-601).  ghosts_only = 1 writes only the border
  * (ghost) slots, which the iteration kernels never write: enough for a fresh

@@ -20,11 +20,16 @@ SBP_POT_BAND, SBP_POT_ELL, SBP_POT_DENSE = 0, 1, 2
 SBP_MAX_R = 32
 SBP_ERR_NONE = 0xFFFFFFFFFFFFFFFF
 SBP_ITER_FIRST = 1
+SBP_ACC_F32, SBP_ACC_F64 = 0, 1
+
+
+SBP_DEVICE_AUTO = -1
 
 
 class SbpGrid(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int), ("W", ctypes.c_int), ("M", ctypes.c_int),
-                ("Ms", ctypes.c_int), ("r0", ctypes.c_int), ("rows", ctypes.c_int)]
+                ("Ms", ctypes.c_int), ("r0", ctypes.c_int), ("rows", ctypes.c_int),
+                ("device", ctypes.c_int)]
 
 
 class SbpPotential(ctypes.Structure):
@@ -35,7 +40,9 @@ class SbpPotential(ctypes.Structure):
                 ("ell_idx", ctypes.c_void_p * 2), ("ell_w", ctypes.c_void_p * 2),
                 ("dense_t", ctypes.c_void_p * 2),
                 ("n_pot", ctypes.c_int), ("fbar_all", ctypes.c_void_p),
-                ("pid_h", ctypes.c_void_p), ("pid_v", ctypes.c_void_p)]
+                ("pid_h", ctypes.c_void_p), ("pid_v", ctypes.c_void_p),
+                ("accumulate", ctypes.c_int), ("fbar64", ctypes.c_double * 2),
+                ("ell_w_lo", ctypes.c_void_p * 2)]
 
 
 class SbpError(RuntimeError):
@@ -58,7 +65,9 @@ _i = ctypes.c_int
 _PROTOS = {
     "sbp_version": (_i, []),
     "sbp_last_error": (ctypes.c_char_p, []),
+    "sbp_reload_config": (_i, []),
     "sbp_padded_labels": (_i, [_i]),
+    "sbp_band_radius": (_i, [_i, _i]),
     "sbp_init_msgs": (_i, [ctypes.POINTER(SbpGrid), _i, _i, _P, _P]),
     "sbp_load_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, _P]),
     "sbp_stereo_values": (_i, [ctypes.POINTER(SbpGrid), _i, _P, _P, ctypes.c_double,

@@ -32,6 +32,9 @@ struct EllArgs {
     long long pot_stride;       // m_max * Ms
     const float *fbar_all;      // per-edge: [n_pot][2], else NULL
     const int *pid_h, *pid_v;   // per-edge potential ids (global nodes), else NULL
+    int acc64;                  // sum-product in f64 (sbp_potential::accumulate)
+    double fbar64[2];
+    const float *w_lo;          // acc64: low f32 plane of the weights (w = w + w_lo)
 };
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s);
 cudaError_t launch_ell_sweep(int domain, const EllArgs &a, cudaStream_t s);

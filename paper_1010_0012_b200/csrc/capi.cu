@@ -7,6 +7,7 @@
 #include "aux_kernels.cuh"
 #include "band_kernel.cuh"
 #include "fused_kernel.cuh"
+#include "tap_kernel.cuh"
 
 namespace sbp {
 template <int MS, int DOM>
@@ -29,6 +30,11 @@ BandLaunchFn pick_chain(int R, int vl);
     extern template FusedLaunchFn pick_fused<MSV, SBP_MAX>(int, bool);
 SBP_EXTERN(8) SBP_EXTERN(16) SBP_EXTERN(32) SBP_EXTERN(64) SBP_EXTERN(128) SBP_EXTERN(256)
 #undef SBP_EXTERN
+#define SBP_EXTERN_TAP(MSV)                                                                  \
+    extern template BandLaunchFn pick_band_tap<MSV, SBP_SUM>(int, int, bool, int);          \
+    extern template BandLaunchFn pick_band_tap<MSV, SBP_MAX>(int, int, bool, int);
+SBP_EXTERN_TAP(64) SBP_EXTERN_TAP(128) SBP_EXTERN_TAP(256)
+#undef SBP_EXTERN_TAP
 }
 
 namespace {
@@ -47,6 +53,17 @@ int fail(int code, const char *fmt, ...) {
 // is independent of the one torch sets.  Every launching entry point
 // therefore selects the device that owns its buffers first; otherwise rank k
 // of a multi-GPU run would launch on device 0 with device k's pointers.
+// sbp_grid::device names it (no driver query per launch); SBP_DEVICE_AUTO
+// falls back to looking it up from a buffer pointer.
+int select_device_of(const void *p);
+int select_device(const sbp_grid *g, const void *p) {
+    if (g->device < 0) return select_device_of(p);
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g->device) cudaSetDevice(g->device);
+    return g->device;
+}
+
 int select_device_of(const void *p) {
     cudaPointerAttributes attr;
     if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
@@ -80,23 +97,68 @@ const int kRadii[] = {1, 2, 3, 4, 7, 8, 16, 32};   // = SBP_BAND_RADII (band_ker
 // Band kernel variant choice, from the B200 A/B runs (tools/ab_vl.sh,
 // tools/ab_staged.sh; profiles/r01_kernel_variants.md).  Environment
 // overrides: SBP_BAND_VL=8|16, SBP_STAGED=0|1, SBP_ROLL_MIN_R=<r>.
-int env_int(const char *name, int dflt) {
+int env_int_raw(const char *name, int dflt) {
     const char *e = getenv(name);
     return e ? atoi(e) : dflt;
 }
 
+// The knobs are read once per process (no getenv on the launch path).
+struct EnvKnobs {
+    int roll_min_r = env_int_raw("SBP_ROLL_MIN_R", -1);
+    int staged = env_int_raw("SBP_STAGED", -1);
+    int band_vl = env_int_raw("SBP_BAND_VL", 0);
+    int fuse_rolled = env_int_raw("SBP_FUSE_ROLLED", 1);
+    int chain_vl = env_int_raw("SBP_CHAIN_VL", 8);
+    int tap = env_int_raw("SBP_TAP", -1);            // shared-memory-tap kernels: 0 off, 1 on
+    int tap_vl = env_int_raw("SBP_TAP_VL", 0);
+    int tap_staged = env_int_raw("SBP_TAP_STAGED", -1);
+    int tap_rolled = env_int_raw("SBP_TAP_ROLLED", -1);
+};
+EnvKnobs &knobs() {
+    static EnvKnobs k;
+    return k;
+}
+int env_int(const char *name, int dflt) {
+    const EnvKnobs &k = knobs();
+    int v = -1;
+    if (!strcmp(name, "SBP_ROLL_MIN_R")) v = k.roll_min_r;
+    else if (!strcmp(name, "SBP_STAGED")) v = k.staged;
+    else if (!strcmp(name, "SBP_BAND_VL")) return k.band_vl;
+    else if (!strcmp(name, "SBP_FUSE_ROLLED")) return k.fuse_rolled;
+    else if (!strcmp(name, "SBP_CHAIN_VL")) return k.chain_vl;
+    else return env_int_raw(name, dflt);
+    return v < 0 ? dflt : v;
+}
+
 struct BandChoice {
     int vl;       // labels per lane
-    int variant;  // 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged (R <= 16)
+    int variant;  // 0 unrolled, 1 rolled (symmetric, R >= 24), 2 TMA-staged (R <= 16),
+                  // 3 shared-memory taps (tap_kernel.cuh; R in {8, 16, 32}, Ms >= 64)
+    int rolled = 0, staged = 0;   // variant 3 only
 };
 
+// Shared-memory-tap kernel for wide bands: default off until the B200 A/B
+// picks it (SBP_TAP=1 forces it where compiled).
+bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
+    const EnvKnobs &k = knobs();
+    const bool compiled = Ms >= 64 && (Rk == 8 || Rk == 16 || Rk == 32);
+    const int dflt = 0;
+    if (!compiled || (k.tap < 0 ? dflt : k.tap) == 0) return false;
+    c.variant = 3;
+    c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
+    if (k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = k.tap_vl;
+    c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym) : (sym && Rk >= 32);
+    c.staged = k.tap_staged >= 0 ? (k.tap_staged && c.vl == 8) : (domain == SBP_MAX && c.vl == 8);
+    return true;
+}
+
 int band_roll_min_r() {
-    static int v = env_int("SBP_ROLL_MIN_R", 24);   // rolled wins at R = 32, loses at R <= 16
-    return v;
+    return env_int("SBP_ROLL_MIN_R", 24);   // rolled wins at R = 32, loses at R <= 16
 }
 
 BandChoice band_choice(int Ms, int domain, int Rk, bool sym) {
     BandChoice c;
+    if (tap_choice(Ms, domain, Rk, sym, c)) return c;
     // packed-FP32 build, B200 A/B (profiles/r01_ab_packed.txt): the rolled
     // VL=16 kernel is the fastest for C4 (sum, Ms=128, R=7) cold and
     // sustained; rolled instantiations exist for R in {4, 7, 8} and R >= 24
@@ -140,8 +202,21 @@ sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled);
 
 // The launch function actually used: the chosen variant if compiled, else
 // the always-compiled register-loaded VL=8 kernel (ch is updated to match).
+sbp::BandLaunchFn tap_fn(int Ms, int dom, int vl, int R, bool rolled, int staged) {
+    switch (Ms) {
+    case 64: return dom == SBP_SUM ? sbp::pick_band_tap<64, SBP_SUM>(vl, R, rolled, staged)
+                                   : sbp::pick_band_tap<64, SBP_MAX>(vl, R, rolled, staged);
+    case 128: return dom == SBP_SUM ? sbp::pick_band_tap<128, SBP_SUM>(vl, R, rolled, staged)
+                                    : sbp::pick_band_tap<128, SBP_MAX>(vl, R, rolled, staged);
+    case 256: return dom == SBP_SUM ? sbp::pick_band_tap<256, SBP_SUM>(vl, R, rolled, staged)
+                                    : sbp::pick_band_tap<256, SBP_MAX>(vl, R, rolled, staged);
+    default: return nullptr;
+    }
+}
+
 sbp::BandLaunchFn band_resolve(int Ms, int dom, int Rk, BandChoice &ch) {
-    sbp::BandLaunchFn fn = band_fn(Ms, dom, ch.vl, Rk, ch.variant);
+    sbp::BandLaunchFn fn = ch.variant == 3 ? tap_fn(Ms, dom, ch.vl, Rk, ch.rolled, ch.staged)
+                                           : band_fn(Ms, dom, ch.vl, Rk, ch.variant);
     if (!fn) {
         ch.vl = 8;
         ch.variant = 0;
@@ -235,6 +310,19 @@ int ell_args(const sbp_grid *g, const sbp_potential *pot, sbp::EllArgs *a) {
         a->pid_h = pot->pid_h;
         a->pid_v = pot->pid_v;
     }
+    if (pot->accumulate == SBP_ACC_F64) {
+        if (pot->domain != SBP_SUM || pot->kind != SBP_POT_ELL || pot->n_pot != 0)
+            return fail(SBP_EUNSUPPORTED,
+                        "f64 accumulation needs a shared sum-product potential in ELL form");
+        if (!pot->ell_w_lo[0] || pot->ell_w_lo[1] != pot->ell_w_lo[0] + ps)
+            return fail(SBP_EINVAL, "f64 accumulation needs the low weight plane ell_w_lo");
+        a->acc64 = 1;
+        a->fbar64[0] = pot->fbar64[0];
+        a->fbar64[1] = pot->fbar64[1];
+        a->w_lo = pot->ell_w_lo[0];
+    } else if (pot->accumulate != SBP_ACC_F32) {
+        return fail(SBP_EINVAL, "bad accumulate %d", pot->accumulate);
+    }
     return SBP_OK;
 }
 
@@ -245,6 +333,18 @@ extern "C" {
 int sbp_version(void) { return 1; }
 
 const char *sbp_last_error(void) { return g_err; }
+
+int sbp_reload_config(void) {
+    knobs() = EnvKnobs();
+    return SBP_OK;
+}
+
+int sbp_band_radius(int Ms, int R) {
+    if (R < 0 || R > SBP_MAX_R) return 0;
+    for (int r : kRadii)
+        if (r >= R && r < Ms) return r;
+    return 0;
+}
 
 int sbp_padded_labels(int M) {
     if (M < 1) return fail(SBP_EINVAL, "M must be >= 1");
@@ -257,7 +357,7 @@ int sbp_padded_labels(int M) {
 int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!msgs) return fail(SBP_EINVAL, "msgs is NULL");
-    select_device_of(msgs);
+    select_device(g, msgs);
     return cuda_status(sbp::launch_init_msgs(msgs, g->H, g->W, g->M, g->Ms, g->r0, g->rows,
                                              domain, ghosts_only ? 1 : 0, (cudaStream_t)stream),
                        "sbp_init_msgs");
@@ -266,7 +366,7 @@ int sbp_init_msgs(const sbp_grid *g, int domain, int ghosts_only, float *msgs, v
 int sbp_load_values(const sbp_grid *g, int domain, const double *src, float *dst, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!src || !dst) return fail(SBP_EINVAL, "NULL pointer");
-    select_device_of(dst);
+    select_device(g, dst);
     return cuda_status(sbp::launch_load_values(src, dst, (long long)g->rows * g->W, g->M, g->Ms,
                                                domain, (cudaStream_t)stream),
                        "sbp_load_values");
@@ -277,7 +377,7 @@ int sbp_stereo_values(const sbp_grid *g, int domain, const uint8_t *left, const 
     if (int rc = check_grid(g)) return rc;
     if (!left || !right || !dst) return fail(SBP_EINVAL, "NULL pointer");
     if (!(beta > 0) || !(T_u > 0)) return fail(SBP_EINVAL, "beta and T_u must be > 0");
-    select_device_of(dst);
+    select_device(g, dst);
     return cuda_status(sbp::launch_stereo_values(left, right, (long long)g->rows, g->W, g->M,
                                                  g->Ms, beta, T_u, domain, dst,
                                                  (cudaStream_t)stream),
@@ -294,10 +394,12 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         return fail(SBP_EINVAL, "bad row range [%d, %d) of %d rows", lr_begin, lr_end, g->rows);
     if (lr_begin == lr_end) return SBP_OK;
     if (iteration < 0 || iteration >= (1 << 23)) return fail(SBP_EINVAL, "bad iteration index");
-    select_device_of(msgs_out);
+    select_device(g, msgs_out);
     const long long slot = (long long)(g->rows + 2) * g->W * g->Ms;
     cudaStream_t s = (cudaStream_t)stream;
     if (pot->kind == SBP_POT_BAND) {
+        if (pot->accumulate != SBP_ACC_F32)
+            return fail(SBP_EUNSUPPORTED, "band kernels accumulate in f32 (plan ELL for f64)");
         if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
         int Rk = 0;
         for (int r : kRadii)
@@ -317,6 +419,8 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
     }
     if (pot->kind == SBP_POT_DENSE && pot->n_pot == 0 && pot->dense_t[0] && pot->dense_t[1] &&
         g->Ms >= 32) {
+        if (pot->accumulate != SBP_ACC_F32)
+            return fail(SBP_EUNSUPPORTED, "the dense kernel accumulates in f32");
         sbp::DenseArgs a;
         a.values = values;
         a.msgs_in = msgs_in;
@@ -367,7 +471,7 @@ int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *
     const int Rk = band_radius(g, pot);
     sbp::FusedLaunchFn fn = Rk ? fused_fn(g->Ms, pot->domain, Rk, fused_rolled(g, pot, Rk)) : nullptr;
     if (!fn) return fail(SBP_EUNSUPPORTED, "no fused kernel for Ms=%d R=%d", g->Ms, pot->R);
-    select_device_of(msgs_a);
+    select_device(g, msgs_a);
     sbp::BandArgs a;
     band_args(g, pot, Rk, values, &a);
     a.err = err;
@@ -397,7 +501,7 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
     if (!pot || !values || !msgs || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "sequential sweeps need the full grid");
     if (sweep < 0 || sweep >= (1 << 23)) return fail(SBP_EINVAL, "bad sweep index");
-    select_device_of(msgs);
+    select_device(g, msgs);
     if (pot->kind != SBP_POT_BAND) {
         sbp::EllArgs a;
         if (int rc = ell_args(g, pot, &a)) return rc;
@@ -410,6 +514,8 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
                            "sbp_sweep(ell)");
     }
     if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
+    if (pot->accumulate != SBP_ACC_F32)
+        return fail(SBP_EUNSUPPORTED, "band kernels accumulate in f32 (plan ELL for f64)");
     int Rk = 0;
     for (int r : kRadii)
         if (r >= pot->R && r < g->Ms) { Rk = r; break; }
@@ -466,14 +572,19 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         } else {
             BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
             if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);
-            snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
-                     ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom, ch.vl,
-                     g->Ms / ch.vl, Rk, ch.variant == 1 ? ",rolled" : "");
+            if (ch.variant == 3)
+                snprintf(buf, len, "band_iter_tap_kernel<%s,VL=%d,LP=%d,R=%d%s%s>", dom, ch.vl,
+                         g->Ms / ch.vl, Rk, ch.rolled ? ",rolled" : "", ch.staged ? ",staged" : "");
+            else
+                snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
+                         ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom,
+                         ch.vl, g->Ms / ch.vl, Rk, ch.variant == 1 ? ",rolled" : "");
         }
     } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
         snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
     } else {
-        snprintf(buf, len, "ell_iter_kernel<%s>", dom);
+        snprintf(buf, len, "%s<%s%s>", sequential == 1 ? "ell_chain_kernel" : "ell_iter_kernel", dom,
+                 pot->accumulate == SBP_ACC_F64 ? ",f64" : "");
     }
     return SBP_OK;
 }
@@ -483,7 +594,7 @@ int sbp_beliefs(const sbp_grid *g, int domain, const float *values, const float 
                 unsigned long long *bad_node, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!values || !msgs) return fail(SBP_EINVAL, "NULL pointer");
-    select_device_of(msgs);
+    select_device(g, msgs);
     return cuda_status(sbp::launch_beliefs(domain, values, msgs, g->W, g->M, g->Ms, g->rows,
                                            beliefs, normalizers, labels, bad_node,
                                            (cudaStream_t)stream),
@@ -494,7 +605,7 @@ int sbp_gather_store(const sbp_grid *g, const float *msgs, float *out, void *str
     if (int rc = check_grid(g)) return rc;
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "gather needs the full grid");
     if (!msgs || !out) return fail(SBP_EINVAL, "NULL pointer");
-    select_device_of(msgs);
+    select_device(g, msgs);
     return cuda_status(sbp::launch_gather_store(msgs, g->H, g->W, g->M, g->Ms, out,
                                                 (cudaStream_t)stream),
                        "sbp_gather_store");
@@ -504,7 +615,7 @@ int sbp_max_abs_diff(const sbp_grid *g, const float *a, const float *b, float *o
                      void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!a || !b || !out) return fail(SBP_EINVAL, "NULL pointer");
-    select_device_of(a);
+    select_device(g, a);
     return cuda_status(sbp::launch_max_abs_diff(a, b, g->W, g->M, g->Ms, g->rows, out,
                                                 (cudaStream_t)stream),
                        "sbp_max_abs_diff");

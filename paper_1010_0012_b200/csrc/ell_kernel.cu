@@ -69,6 +69,69 @@ __device__ __forceinline__ void ell_h(const float (&g)[ELL_QMAX], const float (&
     }
 }
 
+// Accurate sum-product (EllArgs::acc64): the exclusion products, S, the floor
+// term, the correction and the normaliser in f64 (the reference's own
+// precision, numba_kernels.py:44-54, 248-258) from the f32-stored inputs;
+// weights carry f64 precision as a hi + lo pair of f32 planes, fbar as f64.
+// Only the stored message is rounded to f32.  For weak smoothing with wide
+// bands, where fp32 accumulation drifts past the 1e-5 parity bar.
+__device__ __forceinline__ void ell_h64(const float (&g)[ELL_QMAX], const float (&m)[4][ELL_QMAX],
+                                        int excl, double (&h)[ELL_QMAX]) {
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) {
+        double v = g[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k != excl) v *= (double)m[k][q];
+        h[q] = v;
+    }
+}
+
+__device__ __forceinline__ bool ell_message64(const EllArgs &a, const double (&h)[ELL_QMAX],
+                                              double *hs, int lane, long long pslot,
+                                              float (&out)[ELL_QMAX]) {
+    double red = 0.0;
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) {
+        const int x = lane + 32 * q;
+        if (x < a.Ms) {
+            hs[x] = h[q];
+            red += h[q];
+        }
+    }
+    for (int off = 16; off; off >>= 1) red += __shfl_xor_sync(SBP_FULL_MASK, red, off);
+    __syncwarp();
+    const double base = a.floor_term ? a.fbar64[pslot & 1] * red : 0.0;
+    const long long off0 = pslot * a.pot_stride;
+    double acc[ELL_QMAX];
+    double tot = 0.0;
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) {
+        const int x = lane + 32 * q;
+        double v = base;
+        if (x < a.M) {
+            const int *ip = a.idx + off0 + x;
+            const float *wp = a.w + off0 + x;
+            const float *lp = a.w_lo + off0 + x;
+            for (int k = 0; k < a.m_max; ++k) {
+                const long long o = (long long)k * a.Ms;
+                const double w = (double)wp[o] + (double)lp[o];
+                v = fma(w, hs[ip[o]], v);
+            }
+        } else {
+            v = 0.0;
+        }
+        acc[q] = v;
+        if (x < a.Ms) tot += v;
+    }
+    __syncwarp();
+    for (int off = 16; off; off >>= 1) tot += __shfl_xor_sync(SBP_FULL_MASK, tot, off);
+    const double inv = 1.0 / tot;
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) out[q] = (float)(acc[q] * inv);
+    return (tot > 0.0) && !isinf(tot);
+}
+
 // The message of one directed edge: floor term + ELL correction (or the dense
 // sum when floor_term = 0 and the lists are full), then normalisation.
 template <int DOM>
@@ -138,11 +201,12 @@ __device__ __forceinline__ void ell_store(const EllArgs &a, float *base, int lan
     }
 }
 
-template <int DOM>
+template <int DOM, int ACC>
 __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_constant__ EllArgs a) {
-    __shared__ float hs_all[ELL_WARPS][32 * ELL_QMAX];
+    __shared__ double hs_all[ELL_WARPS][32 * ELL_QMAX];
     const int lane = threadIdx.x & 31;
-    float *hs = hs_all[threadIdx.x >> 5];
+    float *hs = reinterpret_cast<float *>(hs_all[threadIdx.x >> 5]);
+    double *hs64 = hs_all[threadIdx.x >> 5];
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (p >= npix) return;   // warp-uniform
@@ -174,9 +238,17 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
 #pragma unroll
     for (int dir = 0; dir < 4; ++dir) {
         if (!has[dir]) continue;
-        float h[ELL_QMAX], out[ELL_QMAX];
-        ell_h<DOM>(g, m, dir_excl(dir), h);
-        const bool ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), out);
+        float out[ELL_QMAX];
+        bool ok;
+        if constexpr (ACC && DOM == SBP_SUM) {
+            double h[ELL_QMAX];
+            ell_h64(g, m, dir_excl(dir), h);
+            ok = ell_message64(a, h, hs64, lane, ell_pot_slot(a, r, c, dir), out);
+        } else {
+            float h[ELL_QMAX];
+            ell_h<DOM>(g, m, dir_excl(dir), h);
+            ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), out);
+        }
         const long long step = dir == 0 ? 1 : dir == 1 ? -1 : dir == 2 ? W : -W;
         ell_store(a, a.msgs_out + dir_wslot(dir) * a.slot_stride + (node_l + step) * a.Ms, lane,
                   out);
@@ -187,11 +259,12 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
 
 // Sequential (canonical) pass over chains, one warp per chain; see
 // chain_kernel.cuh for the pass geometry and the failure key.
-template <int DOM>
+template <int DOM, int ACC>
 __global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_constant__ EllArgs a) {
-    __shared__ float hs_all[ELL_WARPS][32 * ELL_QMAX];
+    __shared__ double hs_all[ELL_WARPS][32 * ELL_QMAX];
     const int lane = threadIdx.x & 31;
-    float *hs = hs_all[threadIdx.x >> 5];
+    float *hs = reinterpret_cast<float *>(hs_all[threadIdx.x >> 5]);
+    double *hs64 = hs_all[threadIdx.x >> 5];
     const int dir = a.pass;
     const long long H = a.H, W = a.W;
     const long long n_lines = dir <= 1 ? H : W, len = dir <= 1 ? W - 1 : H - 1;
@@ -223,11 +296,18 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_
                 m[k][q] = k == wslot ? chain[q]
                         : (k == excl || !in) ? PAD : msgs[k * S + (src + W) * a.Ms + x];
         }
-        float h[ELL_QMAX];
-        ell_h<DOM>(g, m, excl, h);
         const long long r = src / W;
         const int c = (int)(src % W);
-        const bool ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), chain);
+        bool ok;
+        if constexpr (ACC && DOM == SBP_SUM) {
+            double h[ELL_QMAX];
+            ell_h64(g, m, excl, h);
+            ok = ell_message64(a, h, hs64, lane, ell_pot_slot(a, r, c, dir), chain);
+        } else {
+            float h[ELL_QMAX];
+            ell_h<DOM>(g, m, excl, h);
+            ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), chain);
+        }
         ell_store(a, msgs + wslot * S + (src + step + W) * a.Ms, lane, chain);
         if (!ok && lane == 0) {
             const unsigned long long key = ((unsigned long long)a.iteration << 40) |
@@ -243,10 +323,12 @@ cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s) {
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long blocks = (npix + ELL_WARPS - 1) / ELL_WARPS;
     if (blocks <= 0) return cudaSuccess;
-    if (domain == SBP_SUM)
-        ell_iter_kernel<SBP_SUM><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
+    if (domain == SBP_SUM && a.acc64)
+        ell_iter_kernel<SBP_SUM, 1><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
+    else if (domain == SBP_SUM)
+        ell_iter_kernel<SBP_SUM, 0><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
     else
-        ell_iter_kernel<SBP_MAX><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
+        ell_iter_kernel<SBP_MAX, 0><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -258,10 +340,12 @@ cudaError_t launch_ell_sweep(int domain, const EllArgs &a, cudaStream_t s) {
         const long long len = dir <= 1 ? a.W - 1 : a.H - 1;
         if (len <= 0) continue;
         const long long blocks = (lines + ELL_WARPS - 1) / ELL_WARPS;
-        if (domain == SBP_SUM)
-            ell_chain_kernel<SBP_SUM><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
+        if (domain == SBP_SUM && a.acc64)
+            ell_chain_kernel<SBP_SUM, 1><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
+        else if (domain == SBP_SUM)
+            ell_chain_kernel<SBP_SUM, 0><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
         else
-            ell_chain_kernel<SBP_MAX><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
+            ell_chain_kernel<SBP_MAX, 0><<<(unsigned)blocks, 32 * ELL_WARPS, 0, s>>>(b);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }

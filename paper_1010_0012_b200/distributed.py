@@ -34,7 +34,8 @@ def run_sweeps_strips(model, n_sweeps: int, domain: str = "sum", kernel: str = "
         strip = GpuStrip(model, r0, rows, domain, kernel, device=device, values=values)
     eng = strip.engine
     eng.reset()
-    interior = torch.cuda.Stream(device=eng.device)
+    cuda = torch.device(eng.device).type == "cuda"
+    interior = torch.cuda.Stream(device=eng.device) if cuda else None
     if world == 1:
         eng.step(n_sweeps)
     else:
@@ -53,6 +54,7 @@ def gather_labels(eng, group=None) -> np.ndarray | None:
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     H, W = eng.H, eng.W
+    lab = lab.to(torch.int32)
     parts = partition_rows(H, world)
     width = max(rows for _, rows in parts) * W
     buf = torch.full((width,), -1, dtype=torch.int32, device=lab.device)

@@ -35,6 +35,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from .model import edge_mapping, model_directed_ids
 from .plan import PotentialPlan, plan_per_edge, plan_potential
 
 __all__ = ["SYNCHRONOUS", "SEQUENTIAL", "DegenerateMessageError", "DegenerateBeliefError",
@@ -163,8 +164,10 @@ def _edge_endpoints(H: int, W: int, d: int) -> tuple[int, int]:
     return (a, b) if d % 2 == 0 else (b, a)
 
 
-def _stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream_handle(device=None) -> int:
+    """The current torch stream of ``device`` (not of the current device: an
+    engine on cuda:1 launches on cuda:1's stream whatever device is current)."""
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def _ptr(t: torch.Tensor) -> int:
@@ -180,7 +183,7 @@ class GridEngine:
 
     def __init__(self, model, domain: str = "sum", kernel: str = "fast", device=None,
                  r0: int = 0, rows: int | None = None, values: np.ndarray | None = None,
-                 schedule: str = SYNCHRONOUS):
+                 schedule: str = SYNCHRONOUS, precision: str | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("the GPU grid engine needs a CUDA device (no CPU fallback)")
         self.lib = L.lib()
@@ -192,6 +195,8 @@ class GridEngine:
         self.domain = domain
         self.kernel = kernel
         self.device = torch.device(device) if device is not None else torch.device("cuda")
+        if self.device.index is None:      # pin the device the engine was created on
+            self.device = torch.device("cuda", torch.cuda.current_device())
         pot = _shared_potential(model) if model.n_edges else None
         for p in (_unique_potentials(model) if model.n_edges else []):
             _validate(model, kernel, domain, p)
@@ -203,11 +208,18 @@ class GridEngine:
         self.Ms = self.lib.sbp_padded_labels(self.M)
         if self.Ms > 256:
             raise NotImplementedError(f"M={self.M} > 256 labels is not supported on the GPU path")
-        self.grid = L.SbpGrid(self.H, self.W, self.M, self.Ms, self.r0, self.rows)
+        self.grid = L.SbpGrid(self.H, self.W, self.M, self.Ms, self.r0, self.rows,
+                              self.device.index)
         self.dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
         self.plan: PotentialPlan | None = None
+        # sum-product accumulation: "auto" (f64 for weak smoothing over wide
+        # bands, plan.wants_f64), "f32" or "f64"; SBP_PRECISION overrides
+        self.precision = precision or os.environ.get("SBP_PRECISION", "auto")
+        if self.precision not in ("auto", "f32", "f64"):
+            raise ValueError(f"precision must be 'auto', 'f32' or 'f64', got {self.precision!r}")
         if pot is not None:
-            self.plan = plan_potential(pot, domain, kernel, self.M, self.Ms)
+            self.plan = plan_potential(pot, domain, kernel, self.M, self.Ms,
+                                       precision=self.precision)
         elif model.n_edges:
             self.plan = plan_per_edge(model, domain, kernel, self.M, self.Ms)
         if self.plan is not None:
@@ -246,12 +258,22 @@ class GridEngine:
                     s.band_w[o][k] = float(v)
         else:
             idx = torch.from_numpy(np.ascontiguousarray(plan.ell_idx)).to(self.device)
-            w = torch.from_numpy(np.ascontiguousarray(plan.ell_w, dtype=np.float32)).to(self.device)
+            hi = np.ascontiguousarray(plan.ell_w, dtype=np.float32)
+            w = torch.from_numpy(hi).to(self.device)
             plan.device_arrays = [idx, w]
             # orientation 1 directly follows orientation 0 ([.., 2, m_max, Ms])
             step = plan.m_max * self.Ms * 4
             s.ell_idx[0], s.ell_idx[1] = idx.data_ptr(), idx.data_ptr() + step
             s.ell_w[0], s.ell_w[1] = w.data_ptr(), w.data_ptr() + step
+            if plan.accumulate == L.SBP_ACC_F64:
+                # f64 weights as hi + lo f32 planes (exact to ~2^-48 relative)
+                with np.errstate(invalid="ignore"):
+                    lo = np.where(np.isfinite(plan.ell_w), plan.ell_w - hi.astype(np.float64), 0.0)
+                wl = torch.from_numpy(np.ascontiguousarray(lo, dtype=np.float32)).to(self.device)
+                plan.device_arrays.append(wl)
+                s.accumulate = L.SBP_ACC_F64
+                s.fbar64[0], s.fbar64[1] = plan.fbar64
+                s.ell_w_lo[0], s.ell_w_lo[1] = wl.data_ptr(), wl.data_ptr() + step
             if plan.n_pot:
                 fb = torch.from_numpy(np.ascontiguousarray(plan.fbar_all, dtype=np.float32)).to(
                     self.device)
@@ -279,7 +301,7 @@ class GridEngine:
             dev.append(t.to(self.device, non_blocking=t.is_pinned()))
         L.check(self.lib.sbp_stereo_values(ctypes_ref(self.grid), self.dom, _ptr(dev[0]),
                                            _ptr(dev[1]), beta, T_u, _ptr(self.values),
-                                           _stream_handle()))
+                                           _stream_handle(self.device)))
         self._staging = dev
 
     def upload_values(self, values: np.ndarray | torch.Tensor | None = None) -> None:
@@ -299,7 +321,7 @@ class GridEngine:
                 host = torch.from_numpy(arr)
             dev = host.to(self.device, non_blocking=host.is_pinned())
         L.check(self.lib.sbp_load_values(ctypes_ref(self.grid), self.dom, _ptr(dev),
-                                         _ptr(self.values), _stream_handle()))
+                                         _ptr(self.values), _stream_handle(self.device)))
         self._staging = dev   # keep alive until the stream consumed it
 
     @property
@@ -316,7 +338,7 @@ class GridEngine:
 
     def _init(self, buf: torch.Tensor, ghosts_only: bool) -> None:
         L.check(self.lib.sbp_init_msgs(ctypes_ref(self.grid), self.dom, 1 if ghosts_only else 0,
-                                       _ptr(buf), _stream_handle()))
+                                       _ptr(buf), _stream_handle(self.device)))
 
     def reset(self, full: bool = False) -> None:
         """Start a new run from the reference initial messages (bp.py:587-601).
@@ -354,7 +376,7 @@ class GridEngine:
             ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
             _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), lr_begin, lr_end,
             self.iterations, L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self.err),
-            _stream_handle() if stream is None else stream))
+            _stream_handle(self.device) if stream is None else stream))
 
     def flip(self) -> None:
         self.cur = 1 - self.cur
@@ -379,7 +401,7 @@ class GridEngine:
             ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
             _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), levels, self.iterations,
             L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self._stamps), self._epoch,
-            self.fuse_lag, self.fuse_rounds, _ptr(self.err), _stream_handle())
+            self.fuse_lag, self.fuse_rounds, _ptr(self.err), _stream_handle(self.device))
         if rc == L.SBP_EUNSUPPORTED:
             self._fused_ok = False
             return False
@@ -394,7 +416,7 @@ class GridEngine:
         if self.plan is not None:
             L.check(self.lib.sbp_sweep(ctypes_ref(self.grid), ctypes_ref(self._pot_struct),
                                        _ptr(self.values), _ptr(self.msgs[0]), self.iterations,
-                                       _ptr(self.err), _stream_handle()))
+                                       _ptr(self.err), _stream_handle(self.device)))
         self.iterations += 1
 
     def snapshot(self) -> None:
@@ -407,11 +429,11 @@ class GridEngine:
                 ev0 = ev1 = None
                 if events is not None:
                     ev0 = torch.cuda.Event(enable_timing=True)
-                    ev0.record()
+                    ev0.record(torch.cuda.current_stream(self.device))
                 self.sweep()
                 if events is not None:
                     ev1 = torch.cuda.Event(enable_timing=True)
-                    ev1.record()
+                    ev1.record(torch.cuda.current_stream(self.device))
                     events.append((ev0, ev1, 1))
             return
         done = 0
@@ -419,21 +441,21 @@ class GridEngine:
             k = min(self.fuse, n - done) if self._can_fuse() else 1
             if events is not None:
                 ev0 = torch.cuda.Event(enable_timing=True)
-                ev0.record()
+                ev0.record(torch.cuda.current_stream(self.device))
             if k < 2 or not self.iterate_fused(k):
                 k = 1
                 self.iterate_rows(1, self.rows + 1)
                 self.flip()
             if events is not None:
                 ev1 = torch.cuda.Event(enable_timing=True)
-                ev1.record()
+                ev1.record(torch.cuda.current_stream(self.device))
                 events.append((ev0, ev1, k))
             done += k
 
     def max_abs_delta(self) -> float:
         out = torch.zeros(1, dtype=torch.float32, device=self.device)
         L.check(self.lib.sbp_max_abs_diff(ctypes_ref(self.grid), _ptr(self.msgs[0]),
-                                          _ptr(self.msgs[1]), _ptr(out), _stream_handle()))
+                                          _ptr(self.msgs[1]), _ptr(out), _stream_handle(self.device)))
         return float(out.item())
 
     def error(self) -> tuple[int, int] | None:
@@ -476,7 +498,7 @@ class GridEngine:
         L.check(self.lib.sbp_beliefs(
             ctypes_ref(self.grid), self.dom, _ptr(self.values), _ptr(self.current),
             _ptr(b) if b is not None else None, _ptr(z) if z is not None else None,
-            _ptr(lab) if lab is not None else None, _ptr(bad), _stream_handle()))
+            _ptr(lab) if lab is not None else None, _ptr(bad), _stream_handle(self.device)))
         return b, z, lab, bad
 
     def labels(self) -> torch.Tensor:
@@ -497,7 +519,7 @@ class GridEngine:
         E = self.H * (self.W - 1) + self.W * (self.H - 1)
         out = torch.empty((2 * E, self.M), dtype=torch.float32, device=self.device)
         L.check(self.lib.sbp_gather_store(ctypes_ref(self.grid), _ptr(self.current), _ptr(out),
-                                          _stream_handle()))
+                                          _stream_handle(self.device)))
         return out
 
     def msgs4(self) -> np.ndarray:
@@ -543,6 +565,11 @@ class MessageStore:
         self.engine = engine
         self._data = data
         self.stats: SweepStats | None = None
+        # a model whose edge list is not in the canonical grid order (the
+        # reference MrfModel accepts any order / orientation): device rows
+        # are canonical and get permuted into the model's directed-edge ids
+        self._mapping = (edge_mapping(model) if getattr(model, "grid_shape", None) is not None
+                         else None)
 
     @property
     def n_directed(self) -> int:
@@ -555,10 +582,22 @@ class MessageStore:
                 fill = 1.0 / self.model.M if self.domain == "sum" else 0.0
                 self._data = np.full((self.n_directed, self.model.M), fill, dtype=np.float64)
             else:
-                self._data = self.engine.store_device().double().cpu().numpy()
+                canon = self.engine.store_device().double().cpu().numpy()
+                if self._mapping is not None:
+                    ids = model_directed_ids(self.model, np.arange(len(canon)), self._mapping)
+                    out = np.empty_like(canon)
+                    out[ids] = canon
+                    canon = out
+                self._data = canon
         return self._data
 
     def edge_id(self, i: int, j: int) -> int:
+        d = self._canonical_edge_id(i, j)
+        if self._mapping is None:
+            return d
+        return int(model_directed_ids(self.model, np.array([d]), self._mapping)[0])
+
+    def _canonical_edge_id(self, i: int, j: int) -> int:
         H, W = self.model.grid_shape
         ri, ci = divmod(int(i), W)
         d = int(j) - int(i)
@@ -566,18 +605,21 @@ class MessageStore:
             e = ri * (2 * W - 1) + (2 * ci if ri < H - 1 else ci)
             return 2 * e
         if d == -1 and ci > 0:
-            return self.edge_id(j, i) + 1
+            return self._canonical_edge_id(j, i) + 1
         if d == W and ri + 1 < H:
             e = ri * (2 * W - 1) + 2 * ci + (1 if ci + 1 < W else 0)
             return 2 * e
         if d == -W and ri > 0:
-            return self.edge_id(j, i) + 1
+            return self._canonical_edge_id(j, i) + 1
         raise KeyError(f"no directed edge {i}->{j} in model")
 
     def vector(self, i: int, j: int) -> np.ndarray:
         return self.data[self.edge_id(i, j)]
 
     def endpoints(self, d: int) -> tuple[int, int]:
+        if self._mapping is not None:
+            a, b = self.model.edges[int(d) // 2]
+            return (int(a), int(b)) if int(d) % 2 == 0 else (int(b), int(a))
         H, W = self.model.grid_shape
         return _edge_endpoints(H, W, int(d))
 
@@ -609,13 +651,17 @@ def _schedule_mode(schedule) -> str:
 
 def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
                schedule=None, convergence_tol: float | None = None, device=None,
-               engine: GridEngine | None = None) -> MessageStore:
+               engine: GridEngine | None = None, precision: str | None = None) -> MessageStore:
     """Run ``n_sweeps`` sweeps on the GPU (reference bp.py:620-703).
 
     ``schedule=None`` -- the reference's canonical in-place sequential sweep;
     ``schedule="synchronous"`` -- one Jacobi iteration per sweep (every
     directed edge once, from the previous iteration's messages only).
     """
+    if getattr(model, "grid_shape", None) is None:
+        raise NotImplementedError(
+            "the GPU engine runs grid models (grid_shape set); the reference's generic "
+            "edge-list engine (bp.py:506-584) is out of scope")
     mode = _schedule_mode(schedule)
     if n_sweeps < 0:
         raise ValueError(f"n_sweeps must be >= 0, got {n_sweeps}")
@@ -627,7 +673,7 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
         store.stats = stats
         return store
     eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device,
-                                                       schedule=mode)
+                                                       schedule=mode, precision=precision)
     if engine is not None or convergence_tol is not None:
         eng.reset(full=convergence_tol is not None)
     per_iter = 2 * int(model.n_edges)

@@ -35,6 +35,8 @@ __all__ = [
     "GridMrf",
     "build_grid_mrf",
     "grid_edges",
+    "MrfModel",
+    "SweepSchedule",
 ]
 
 
@@ -345,3 +347,235 @@ def build_grid_mrf(height: int, width: int, M: int, unary_provider, pairwise,
 
     lu = collect(log_unary_provider) if log_unary_provider is not None else None
     return GridMrf(height, width, M, collect(unary_provider), pairwise, log_unaries=lu)
+
+
+def _grid_edge_keys(height: int, width: int) -> np.ndarray:
+    """Canonical grid edges as sorted keys a * N + b (a < b), in canonical order."""
+    e = grid_edges(height, width)
+    return e[:, 0] * (height * width) + e[:, 1]
+
+
+class MrfModel(GridMrf):
+    """The reference constructor ``MrfModel(M, unaries, edges, potentials,
+    grid_shape=None, log_unaries=None)`` (``mrf.py:298-369``).
+
+    Validation follows the reference (same checks, same messages), with the
+    grid-topology check vectorised (the reference builds two Python edge sets,
+    ``mrf.py:341-348``).  A grid model keeps the caller's edge list and
+    potential list as given; internally it also holds them in the canonical
+    grid order (``canonical_potentials``, ``edge_perm`` / ``edge_flip``) so the
+    GPU engine runs on its fixed layout and ``MessageStore`` maps its rows back
+    to the caller's edge ids (2e: a->b, 2e+1: b->a, bp.py:113-133).
+
+    A model without ``grid_shape`` constructs (the reference's generic
+    engine handles it), but the GPU path serves grid models only and raises
+    ``NotImplementedError`` at ``run_sweeps``.
+    """
+
+    def __init__(self, M: int, unaries, edges, potentials, grid_shape=None, log_unaries=None):
+        if not isinstance(M, (int, np.integer)) or M < 1:
+            raise ValueError(f"label count must be a positive integer, got {M!r}")
+        u = np.ascontiguousarray(unaries, dtype=np.float64)
+        if u.ndim != 2 or u.shape[1] != M:
+            raise ValueError(f"unaries must be (n_nodes, {M}), got {u.shape}")
+        if not np.isfinite(u).all():
+            raise ValueError("unary tables must be finite")
+        if (u < 0).any():
+            raise ValueError("unary tables must be nonnegative")
+        if u.shape[0] == 0:
+            raise ValueError("model needs at least one node")
+        if not (u > 0).any(axis=1).all():
+            bad = int(np.flatnonzero(~(u > 0).any(axis=1))[0])
+            raise ValueError(f"unary table of node {bad} has no positive entry")
+        n = u.shape[0]
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        if e.size:
+            if e.min() < 0 or e.max() >= n:
+                raise ValueError("edge endpoint out of range")
+            if (e[:, 0] == e[:, 1]).any():
+                raise ValueError("self-edges are not allowed")
+            canon = np.sort(e, axis=1)
+            if len(np.unique(canon, axis=0)) != len(canon):
+                raise ValueError("duplicate edges are not allowed")
+        if hasattr(potentials, "M") and (hasattr(potentials, "col_indptr")
+                                         or hasattr(potentials, "table")):
+            shared = potentials
+            pots = [potentials] * len(e)
+        else:
+            pots = list(potentials)
+            shared = pots[0] if pots and all(p is pots[0] for p in pots) else None
+        if len(pots) != len(e):
+            raise ValueError(f"need one potential per edge ({len(e)}), got {len(pots)}")
+        for p in pots:
+            if p.M != M:
+                raise ValueError(f"potential label count {p.M} != model label count {M}")
+        lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+        if grid_shape is not None:
+            h, w = (int(v) for v in grid_shape)
+            if h * w != n:
+                raise ValueError(f"grid {h}x{w} does not match {n} nodes")
+            want = _grid_edge_keys(h, w)
+            keys = lo * n + hi
+            order = np.argsort(keys, kind="stable")
+            if len(keys) != len(want) or not np.array_equal(keys[order], np.sort(want)):
+                raise ValueError("grid topology requires exactly the 4-connected neighbor edges")
+            # canonical position of every model edge (want is already sorted:
+            # node-major, (n, n+1) before (n, n+W))
+            perm = np.empty(len(e), dtype=np.int64)
+            perm[order] = np.arange(len(e))
+            flip = (e[:, 0] > e[:, 1])
+            identity = bool((perm == np.arange(len(e))).all() and not flip.any())
+            if shared is not None:
+                # one shared potential: the reference grid engine, whose
+                # orientation is fixed by the pass direction (bp.py:466-489)
+                canon_pot = shared
+            else:
+                # per-edge: the generic engine orients each potential by its
+                # edge's (a, b) (bp.py:520-541); a reversed edge is the
+                # canonical edge with the transposed potential
+                canon_pot = [None] * len(e)
+                tcache: dict = {}
+                for k in range(len(e)):
+                    p = pots[k]
+                    if flip[k] and hasattr(p, "col_indptr"):
+                        p = tcache.setdefault(id(p), p.transpose())
+                    elif flip[k]:
+                        p = tcache.setdefault(id(p), DensePotential(p.table.T))
+                    canon_pot[perm[k]] = p
+            super().__init__(h, w, M, u, canon_pot, log_unaries=log_unaries)
+            self.edge_perm = None if identity else perm
+            self.edge_flip = None if identity else flip
+        else:
+            if log_unaries is not None:
+                log_unaries = np.ascontiguousarray(log_unaries, dtype=np.float64)
+                if log_unaries.shape != u.shape:
+                    raise ValueError("log_unaries shape must match unaries")
+                log_unaries.setflags(write=False)
+            self.M = int(M)
+            self.grid_shape = None
+            self.unaries = _frozen(u)
+            self._log_unaries = log_unaries
+            self.shared_potential = None
+            self._per_edge = pots
+            self.edge_perm = None
+            self.edge_flip = None
+        self._model_edges = _frozen(e)
+        self._model_pots = pots
+
+    @property
+    def n_edges(self) -> int:
+        return len(self._model_edges)
+
+    @property
+    def edges(self) -> np.ndarray:
+        return self._model_edges
+
+    @property
+    def potentials(self) -> Sequence:
+        return self._model_pots
+
+    @property
+    def canonical_potentials(self) -> Sequence:
+        """Potentials in the canonical grid edge order (GridMrf semantics)."""
+        return GridMrf.potentials.fget(self)
+
+    def __repr__(self) -> str:
+        topo = f"grid{self.grid_shape}" if self.grid_shape else "generic"
+        return f"MrfModel(M={self.M}, nodes={self.n_nodes}, edges={self.n_edges}, {topo})"
+
+
+class SweepSchedule:
+    """Reference ``SweepSchedule`` (bp.py:190-211): ordered directional passes
+    of directed-edge ids.  The GPU path runs the canonical grid schedule
+    (``grid_canonical``) as in-place sequential sweeps; custom pass orders
+    are not supported on the GPU and raise at ``run_sweeps``."""
+
+    def __init__(self, passes, grid_canonical: bool = False):
+        self.passes = [np.asarray(p, dtype=np.int64) for p in passes]
+        self.grid_canonical = grid_canonical
+
+    @classmethod
+    def canonical(cls, model) -> "SweepSchedule":
+        if model.grid_shape is not None:
+            return cls(_grid_passes(model), grid_canonical=True)
+        ne = model.n_edges
+        forward = np.arange(ne, dtype=np.int64) * 2
+        backward = np.arange(ne - 1, -1, -1, dtype=np.int64) * 2 + 1
+        return cls([np.concatenate([forward, backward])])
+
+    @property
+    def n_updates_per_sweep(self) -> int:
+        return sum(len(p) for p in self.passes)
+
+
+def edge_mapping(model):
+    """(perm, flip) of a grid model whose edge list is not the canonical one
+    (model edge k is canonical edge perm[k], given as (b, a) where flip[k]),
+    or None for the canonical order.  Works for this package's models
+    (precomputed) and for any object with ``edges`` / ``grid_shape``, e.g. the
+    reference's own ``MrfModel``."""
+    if isinstance(model, GridMrf) and not isinstance(model, MrfModel):
+        return None
+    if hasattr(model, "edge_perm"):
+        return None if model.edge_perm is None else (model.edge_perm, model.edge_flip)
+    h, w = model.grid_shape
+    e = np.asarray(model.edges, dtype=np.int64).reshape(-1, 2)
+    n = h * w
+    keys = np.minimum(e[:, 0], e[:, 1]) * n + np.maximum(e[:, 0], e[:, 1])
+    want = _grid_edge_keys(h, w)
+    if len(keys) == len(want) and np.array_equal(keys, want) and not (e[:, 0] > e[:, 1]).any():
+        return None
+    order = np.argsort(keys, kind="stable")
+    perm = np.empty(len(e), dtype=np.int64)
+    perm[order] = np.arange(len(e))
+    return perm, e[:, 0] > e[:, 1]
+
+
+def canonical_edge_potentials(model) -> list:
+    """Per-edge potentials in the canonical grid edge order; a reversed edge
+    (b, a) contributes its potential transposed (the generic engine orients a
+    potential by its edge, bp.py:520-541)."""
+    if hasattr(model, "canonical_potentials"):
+        return list(model.canonical_potentials)
+    pots = list(model.potentials)
+    mp = edge_mapping(model)
+    if mp is None:
+        return pots
+    perm, flip = mp
+    out = [None] * len(pots)
+    tcache: dict = {}
+    for k, p in enumerate(pots):
+        if flip[k]:
+            p = tcache.setdefault(id(p), p.transpose() if hasattr(p, "col_indptr")
+                                  else DensePotential(np.asarray(p.table).T))
+        out[perm[k]] = p
+    return out
+
+
+def model_directed_ids(model, canon_ids: np.ndarray, mapping="auto") -> np.ndarray:
+    """Canonical directed-edge ids -> ids in the model's own edge order."""
+    mp = edge_mapping(model) if mapping == "auto" else mapping
+    if mp is None:
+        return canon_ids
+    perm, flip = mp
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(perm))
+    e = inv[canon_ids // 2]
+    return 2 * e + ((canon_ids % 2) ^ flip[e].astype(np.int64))
+
+
+def _grid_passes(model) -> list:
+    """Directed-edge ids of the four canonical passes (bp.py:214-234), vectorised."""
+    h, w = model.grid_shape
+    n = np.arange(h * w, dtype=np.int64).reshape(h, w)
+    ce = np.full((h, w, 2), -1, dtype=np.int64)      # canonical edge of (n, n+1) / (n, n+W)
+    valid = np.zeros((h, w, 2), dtype=bool)
+    valid[:, :-1, 0] = True
+    valid[:-1, :, 1] = True
+    ce[valid] = np.arange(int(valid.sum()))
+    l2r = 2 * ce[:, :-1, 0].ravel()
+    r2l = 2 * ce[:, ::-1, 0][:, 1:].ravel() + 1
+    t2b = 2 * ce[:-1, :, 1].T.ravel()
+    b2t = 2 * ce[::-1, :, 1][1:].T.ravel() + 1
+    del n
+    return [model_directed_ids(model, p) for p in (l2r, r2l, t2b, b2t)]

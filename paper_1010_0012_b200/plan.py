@@ -51,6 +51,8 @@ class PotentialPlan:
     pid_h: np.ndarray | None = None         # (H*W,) int32, potential of edge (n, n+1)
     pid_v: np.ndarray | None = None         # (H*W,) int32, potential of edge (n, n+W)
     madds_per_sweep: int | None = None      # per-edge: the reference counter summed over edges
+    accumulate: int = 0                     # SBP_ACC_F64: f64 sum-product (ELL kind)
+    fbar64: tuple = (0.0, 0.0)
     device_arrays: list = field(default_factory=list)
 
     @property
@@ -153,8 +155,9 @@ def plan_per_edge(model, domain: str, kernel: str, M: int, Ms: int) -> Potential
     unique = []
     pid_h = np.full(H * W, -1, dtype=np.int32)
     pid_v = np.full(H * W, -1, dtype=np.int32)
-    edges = np.asarray(model.edges)
-    pots = list(model.potentials)
+    from .model import canonical_edge_potentials, grid_edges
+    edges = grid_edges(H, W)
+    pots = canonical_edge_potentials(model)
     for (a, b), pot in zip(edges, pots):
         k = uid.setdefault(id(pot), len(unique))
         if k == len(unique):
@@ -191,8 +194,43 @@ def plan_per_edge(model, domain: str, kernel: str, M: int, Ms: int) -> Potential
                          madds_per_update=0, madds_per_sweep=per_sweep)
 
 
+# effective band width above which sum-product accumulates in f64 (auto)
+ACC64_MIN_EFFECTIVE_TAPS = 12.0
+
+
+def effective_taps(pot) -> float:
+    """Mean over columns of sum(residuals) / max(residual): how many stored
+    entries carry weight comparable to the largest.  Truncated linear
+    alpha=0.5 (every BASELINE config): ~4; alpha=0.1, T=33: ~19."""
+    indptr = np.asarray(pot.col_indptr)
+    res = np.abs(np.asarray(pot.col_residuals, dtype=np.float64))
+    lens = np.diff(indptr)
+    if res.size == 0:
+        return 0.0
+    cols = np.repeat(np.arange(len(lens)), lens)
+    tot = np.bincount(cols, weights=res, minlength=len(lens))
+    mx = np.zeros(len(lens))
+    np.maximum.at(mx, cols, res)
+    ok = mx > 0
+    return float((tot[ok] / mx[ok]).mean()) if ok.any() else 0.0
+
+
+def wants_f64(pot, domain: str, kernel: str, precision: str) -> bool:
+    """Accumulation precision of a sum-product run:
+    fp32 accumulation drifts past 1e-5 for weak smoothing over wide bands
+    (5.1e-5 at alpha=0.1, T=33, M=256, 20 iterations), so those potentials --
+    many comparable taps -- accumulate in f64 ("auto"); "f32" / "f64" force."""
+    if domain != "sum" or kernel == "standard" or not _is_sparse(pot):
+        return False
+    if precision == "f64":
+        return True
+    if precision == "f32":
+        return False
+    return effective_taps(pot) > ACC64_MIN_EFFECTIVE_TAPS
+
+
 def plan_potential(pot, domain: str, kernel: str, M: int, Ms: int,
-                   allow_band: bool = True) -> PotentialPlan:
+                   allow_band: bool = True, precision: str = "auto") -> PotentialPlan:
     dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
     pad = 0.0 if domain == "sum" else -np.inf
     use = pot.to_log() if domain == "max" else pot
@@ -220,11 +258,19 @@ def plan_potential(pot, domain: str, kernel: str, M: int, Ms: int,
         floor = 0
     fbar = (float(orients[0].fbar), float(orients[1].fbar))
     madds = madds_per_update(pot, kernel, M)
+    if wants_f64(pot, domain, kernel, precision):
+        m_max, idx, w = _ell(weights, Ms, pad)
+        return PotentialPlan(L.SBP_POT_ELL, dom, kernel, floor, M, Ms, fbar, m_max=m_max,
+                             ell_idx=idx, ell_w=w, madds_per_update=madds,
+                             accumulate=L.SBP_ACC_F64, fbar64=fbar)
     if allow_band:
         bands = [toeplitz_band(sp.col_indptr, sp.col_indices, wt, M, pad) for sp, wt in weights]
         if all(b is not None for b in bands):
             R = max(b[0] for b in bands)
-            if R <= MAX_BAND_R and (R < Ms or R == 0):
+            # a band runs on the smallest compiled radius >= R below Ms; with
+            # none compiled (e.g. Ms = 16, R = 9..15) the general ELL kernel
+            # serves it (same arithmetic order, ascending x_i per column)
+            if R <= MAX_BAND_R and (R == 0 or L.lib().sbp_band_radius(Ms, R) > 0):
                 bw = np.full((2, 2 * R + 1), pad)
                 for o, (r, wv) in enumerate(bands):
                     bw[o, R - r:R + r + 1] = wv

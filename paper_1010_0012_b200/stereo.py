@@ -1,8 +1,9 @@
 """Stereo front end: image pair -> grid MRF whose unaries are built on the GPU.
 
 Mirrors the reference's stereo API (``sparsebp.stereo``, stereo.py:28-140):
-``GrayImage``, ``StereoParams``, ``build_stereo_mrf``, ``stereo_unary_field``,
-``disparity_to_image``.  The model returned by ``build_stereo_mrf`` carries the
+``GrayImage``, ``StereoParams``, ``build_stereo_mrf``, ``stereo_unary_field``
+(the PGM rendering helper ``disparity_to_image`` is out of scope).
+The model returned by ``build_stereo_mrf`` carries the
 image pair; the engine uploads the two uint8 images (2 bytes per pixel) and
 computes the (H*W, M) unary table on the device (``sbp_stereo_values``,
 SURVEY 8f #3) instead of shipping 8*M bytes per pixel of host f64 unaries.
@@ -21,7 +22,7 @@ from .synth import random_dot_pair as _random_dot_pair
 from .synth import stereo_unary_field as _unary_field
 
 __all__ = ["GrayImage", "StereoParams", "StereoMrf", "build_stereo_mrf", "stereo_unary_field",
-           "disparity_to_image", "random_dot_pair"]
+           "random_dot_pair"]
 
 
 @dataclass(frozen=True, eq=False)
@@ -133,17 +134,6 @@ def build_stereo_mrf(left, right, params: StereoParams) -> StereoMrf:
         raise ValueError(f"M={params.M} exceeds image width {R.shape[1]}")
     pot = truncated_linear_potential(params.M, params.alpha, params.T_b)
     return StereoMrf(np.ascontiguousarray(L), np.ascontiguousarray(R), params, pot)
-
-
-def disparity_to_image(labels, M: int, height: int, width: int) -> GrayImage:
-    """round(label * 255 / max(M-1, 1)), half up (reference stereo.py:143-154)."""
-    labels = np.asarray(labels)
-    if labels.size != height * width:
-        raise ValueError(f"expected {height * width} labels, got {labels.size}")
-    if labels.size and (labels.min() < 0 or labels.max() >= M):
-        raise ValueError(f"labels must lie in [0, {M})")
-    scaled = np.floor(labels.astype(np.float64) * (255.0 / max(M - 1, 1)) + 0.5)
-    return GrayImage(scaled.astype(np.uint8).reshape(height, width))
 
 
 def random_dot_pair(height: int, width: int, disparity, seed: int = 0, levels: int = 256):

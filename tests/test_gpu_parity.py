@@ -419,3 +419,18 @@ def test_reference_shaped_model_object(schedule):
         a = sbp.run_sweeps(ref_like, 6, domain=domain, schedule=schedule).data
         b = sbp.run_sweeps(base, 6, domain=domain, schedule=schedule).data
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,domain,variant", [
+    ("C5_T33", "sum", {"SBP_TAP_ROLLED": "1"}), ("C5_T33", "max", {"SBP_TAP_ROLLED": "1"}),
+    ("C5_T17", "max", {"SBP_TAP_STAGED": "1"}), ("C5_T17", "sum", {"SBP_TAP_STAGED": "0"}),
+    ("C5_T9", "max", {"SBP_TAP_STAGED": "0", "SBP_TAP_ROLLED": "0"}),
+])
+def test_tap_and_shuffle_kernels_agree_bitwise(tmp_path, name, domain, variant):
+    """The shared-memory-tap kernels (tap_kernel.cuh) only change how a lane
+    reads its neighbours' h values: same lane width => identical bits."""
+    a = _run_subprocess({"SBP_TAP": "1", "SBP_TAP_VL": "8", **variant}, name, domain, 7,
+                        tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_TAP": "0", "SBP_BAND_VL": "8", "SBP_STAGED": "0",
+                         "SBP_ROLL_MIN_R": "99"}, name, domain, 7, tmp_path / "b.npy")
+    np.testing.assert_array_equal(a, b)

@@ -34,8 +34,8 @@ def test_library_exports_every_header_symbol():
 
 
 def test_struct_layout_matches_header():
-    # sbp_grid: 6 ints; sbp_potential: 5 ints, 2 floats, 2x65 floats, 6 pointers
-    assert ctypes.sizeof(L.SbpGrid) == 24
+    # sbp_grid: 7 ints; sbp_potential: 5 ints, 2 floats, 2x65 floats, 6 pointers
+    assert ctypes.sizeof(L.SbpGrid) == 28
     assert L.SbpPotential.fbar.offset == 20
     assert L.SbpPotential.band_w.offset == 28
     assert L.SbpPotential.ell_idx.offset == 28 + 2 * 65 * 4 + 4  # 8-byte pointer alignment
@@ -215,11 +215,12 @@ def _band_structs(cfg_name, domain):
     class _E:   # the fields _make_pot_struct reads for a band plan
         dom = L.SBP_SUM if domain == "sum" else L.SBP_MAX
     s = engine.GridEngine._make_pot_struct(_E(), pl)
-    g = L.SbpGrid(cfg.height, cfg.width, cfg.M, Ms, 0, cfg.height)
+    g = L.SbpGrid(cfg.height, cfg.width, cfg.M, Ms, 0, cfg.height, L.SBP_DEVICE_AUTO)
     return g, s, pl
 
 
 def _plan_name(cfg_name, domain, sequential=False):
+    L.lib().sbp_reload_config()      # the knobs are read once per process
     g, s, _ = _band_structs(cfg_name, domain)
     buf = ctypes.create_string_buffer(128)
     mode = {False: 0, True: 1}.get(sequential, sequential)
