@@ -26,6 +26,8 @@
  *                                            `compute_max_marginals`, `map_labels`
  *   sbp_gather_store   <- bp.py:604-617      `_grid_store_to_messages`
  *   sbp_max_abs_diff   <- bp.py:671-676      convergence test of `run_sweeps`
+ *                         (sbp_iterate_delta / sbp_sweep_delta fuse it into the
+ *                         iteration; this separate pass serves the dense kernel)
  *
  * Device layout:
  *   values  [rows][W][Ms]          f32, labels >= M padded (0 sum / -inf max)
@@ -158,6 +160,18 @@ SBP_API int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float
                         const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
                         int iteration, int flags, unsigned long long *err, void *stream);
 
+/* sbp_iterate with the convergence test of run_sweeps fused in (bp.py:671-676,
+ * `delta = |msgs4 - prev|.max()`): every written message is compared with
+ * the value it replaces (msgs_in at the same slot; the reference initial
+ * message at iteration 0) and *delta (device float, zeroed by the caller)
+ * is max-updated.  The old values are the ones the neighbouring nodes read
+ * in the same pass, so they come from L2, not a second HBM pass.  Band and
+ * ELL potentials; the dense comparison kernel returns SBP_EUNSUPPORTED. */
+SBP_API int sbp_iterate_delta(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                              const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                              int iteration, int flags, unsigned long long *err, float *delta,
+                              void *stream);
+
 /* `levels` (1..4) consecutive synchronous iterations over the whole strip in
  * ONE persistent cooperative launch (temporal blocking: a row wavefront with
  * `lag` rows between levels; the intermediate messages stay in L2 and are
@@ -183,6 +197,12 @@ SBP_API int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const
  * warp-per-chain ELL kernel. */
 SBP_API int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values,
                       float *msgs, int sweep, unsigned long long *err, void *stream);
+
+/* sbp_sweep with the fused convergence test (see sbp_iterate_delta): each
+ * message written in place is compared with the value it overwrites. */
+SBP_API int sbp_sweep_delta(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                            float *msgs, int sweep, unsigned long long *err, float *delta,
+                            void *stream);
 
 /* Name of the kernel instantiation sbp_iterate (sequential = 0), sbp_sweep
  * (sequential = 1) or sbp_iterate_fused (sequential = 2; falls back to the

@@ -74,6 +74,10 @@ _PROTOS = {
                                ctypes.c_double, _P, _P]),
     "sbp_iterate": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
                          _i, _i, _i, _i, _P, _P]),
+    "sbp_iterate_delta": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P,
+                               _P, _i, _i, _i, _i, _P, _P, _P]),
+    "sbp_sweep_delta": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _i,
+                             _P, _P, _P]),
     "sbp_fused_stamp_words": (_i, [ctypes.POINTER(SbpGrid)]),
     "sbp_iterate_fused": (_i, [ctypes.POINTER(SbpGrid), ctypes.POINTER(SbpPotential), _P, _P, _P,
                                _i, _i, _i, _P, ctypes.c_uint, _i, _i, _P, _P]),

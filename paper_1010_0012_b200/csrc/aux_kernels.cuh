@@ -35,6 +35,7 @@ struct EllArgs {
     int acc64;                  // sum-product in f64 (sbp_potential::accumulate)
     double fbar64[2];
     const float *w_lo;          // acc64: low f32 plane of the weights (w = w + w_lo)
+    float *delta;               // fused convergence test (BandArgs::delta), NULL: off
 };
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s);
 cudaError_t launch_ell_sweep(int domain, const EllArgs &a, cudaStream_t s);

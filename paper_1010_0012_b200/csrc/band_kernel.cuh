@@ -53,6 +53,12 @@ struct BandArgs {
     // Pair table for the packed band: wp[o][k] = (w(k-R-1), w(k-R-2)), with
     // w(d) = pad (0 / -inf) for |d| > R, R the compiled radius (band_pairs()).
     float2 wp[2][2 * SBP_MAX_R + 4];
+    // Fused convergence test (bp.py:671-676): when set, every written message
+    // also compares itself with the value it replaces in the previous
+    // iteration's buffer (the same slot of msgs_in; in place for sweeps) and
+    // the kernel max-reduces |new - old| into *delta (non-negative floats
+    // compare as ints: atomicMax on the bits).  NULL: off.
+    float *delta;
 };
 
 // Fills BandArgs::wp from BandArgs::w for the compiled radius R.
@@ -73,10 +79,47 @@ struct IterCtx {
     const float *msgs_in;
     float *msgs_out;
     int lr_begin, iteration, first;
+    float *dmax;   // this thread's running max |new - old| (BandArgs::delta)
 };
 
-__device__ __forceinline__ IterCtx iter_of(const BandArgs &a) {
-    return IterCtx{a.msgs_in, a.msgs_out, a.lr_begin, a.iteration, a.first};
+__device__ __forceinline__ IterCtx iter_of(const BandArgs &a, float *dmax = nullptr) {
+    return IterCtx{a.msgs_in, a.msgs_out, a.lr_begin, a.iteration, a.first, dmax};
+}
+
+// Largest |out - old| over a lane's labels, old = the message this one
+// replaces (iteration 0: the reference initial message, bp.py:587-601).
+// Padded labels give 0 (sum: 0 - 0) or NaN (max: -inf - -inf), which fmaxf
+// drops.  `src` points at the old value (plain load: in place for sweeps).
+template <int DOM, int VL>
+__device__ __forceinline__ float message_delta(const float (&out)[VL], const float *src,
+                                               bool first, int x0, int M) {
+    float old[VL];
+    if (first) {
+#pragma unroll
+        for (int i = 0; i < VL; ++i)
+            old[i] = x0 + i < M ? (DOM == SBP_SUM ? 1.0f / (float)M : 0.0f) : out[i];
+    } else {
+#pragma unroll
+        for (int c = 0; c < VL / 8; ++c) {
+            const float *p = src + 8 * c;
+            asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=f"(old[8 * c + 0]), "=f"(old[8 * c + 1]), "=f"(old[8 * c + 2]),
+                           "=f"(old[8 * c + 3]), "=f"(old[8 * c + 4]), "=f"(old[8 * c + 5]),
+                           "=f"(old[8 * c + 6]), "=f"(old[8 * c + 7])
+                         : "l"(p));
+        }
+    }
+    float d = 0.0f;
+#pragma unroll
+    for (int i = 0; i < VL; ++i) d = fmaxf(d, fabsf(out[i] - old[i]));
+    return d;
+}
+
+// End of a delta-enabled launch: one atomic per warp.
+__device__ __forceinline__ void flush_delta(float *delta, float dmax) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) dmax = fmaxf(dmax, __shfl_xor_sync(SBP_FULL_MASK, dmax, off));
+    if ((threadIdx.x & 31) == 0 && dmax > 0.0f) atomicMax(reinterpret_cast<int *>(delta), __float_as_int(dmax));
 }
 
 template <int N>
@@ -404,6 +447,9 @@ __device__ __forceinline__ void emit_direction(const BandArgs &a, const IterCtx 
     const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
     const long long dir_off = dir_wslot(DIR) * a.slot_stride + step * a.Ms;
     float *dst = it.msgs_out + (node_l * a.Ms + x0) + dir_off;
+    if (a.delta)
+        *it.dmax = fmaxf(*it.dmax, message_delta<DOM, VL>(out, it.msgs_in + (node_l * a.Ms + x0) + dir_off,
+                                                         it.first, x0, a.M));
     Vec8Loader<VL>::store(dst, out);
     if (!ok && j == 0) report_failure(a.err, it.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
@@ -679,7 +725,8 @@ template <int DOM, int VL, int LP, int R, int NS>
 __global__ void __launch_bounds__(32 * STG_WARPS)
 band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
-    const IterCtx it = iter_of(a);
+    float dmax = 0.0f;
+    const IterCtx it = iter_of(a, &dmax);
     constexpr int VEC = 32 * VL;                 // floats of one vector for one group
     extern __shared__ __align__(128) float stg_smem[];
     __shared__ __align__(8) unsigned long long bars[STG_WARPS][2];
@@ -761,6 +808,7 @@ band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
         band_group_body<DOM, VL, LP, R>(a, it, g, m0, m1, m2, m3, j, x0, valid, node_l, r, c);
         if (NS == 2) st ^= 1;
     }
+    if (a.delta) flush_delta(a.delta, dmax);
 }
 
 template <int DOM, int VL, int LP, int R, int NS>
@@ -799,7 +847,8 @@ template <int DOM, int VL, int LP, int R, bool ROLLED>
 __global__ void __launch_bounds__(128, (VL == 8 ? (DOM == SBP_SUM && R <= 7 ? 6 : 4) : (R <= 8 ? SBP_VL16_BLOCKS : 3)))
 band_iter_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
-    const IterCtx it = iter_of(a);
+    float dmax = 0.0f;
+    const IterCtx it = iter_of(a, &dmax);
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long ngroups = (npix + PPW - 1) / PPW;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -808,6 +857,7 @@ band_iter_kernel(const __grid_constant__ BandArgs a) {
         if constexpr (ROLLED) band_group_rolled<DOM, VL, LP, R>(a, it, grp, npix);
         else band_group<DOM, VL, LP, R>(a, it, grp, npix);
     }
+    if (a.delta) flush_delta(a.delta, dmax);
 }
 
 }  // namespace sbp

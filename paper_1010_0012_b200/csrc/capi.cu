@@ -148,7 +148,10 @@ bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
     if (k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = k.tap_vl;
     c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym) : (sym && Rk >= 32);
-    c.staged = k.tap_staged >= 0 ? (k.tap_staged && c.vl == 8) : (domain == SBP_MAX && c.vl == 8);
+    // staged: 0 register-loaded inputs, 1 TMA-staged inputs, 2 register-light
+    // v2 (all four exclusion vectors in shared-memory rows); VL = 8 only
+    c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0)
+                                 : (domain == SBP_MAX && c.vl == 8 ? 1 : 0);
     return true;
 }
 
@@ -384,9 +387,31 @@ int sbp_stereo_values(const sbp_grid *g, int domain, const uint8_t *left, const 
                        "sbp_stereo_values");
 }
 
+static int iterate_impl(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                        const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                        int iteration, int flags, unsigned long long *err, float *delta,
+                        void *stream);
+
 int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values,
                 const float *msgs_in, float *msgs_out, int lr_begin, int lr_end, int iteration,
                 int flags, unsigned long long *err, void *stream) {
+    return iterate_impl(g, pot, values, msgs_in, msgs_out, lr_begin, lr_end, iteration, flags, err,
+                        nullptr, stream);
+}
+
+int sbp_iterate_delta(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                      const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                      int iteration, int flags, unsigned long long *err, float *delta,
+                      void *stream) {
+    if (!delta) return fail(SBP_EINVAL, "delta is NULL");
+    return iterate_impl(g, pot, values, msgs_in, msgs_out, lr_begin, lr_end, iteration, flags, err,
+                        delta, stream);
+}
+
+static int iterate_impl(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                        const float *msgs_in, float *msgs_out, int lr_begin, int lr_end,
+                        int iteration, int flags, unsigned long long *err, float *delta,
+                        void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!pot || !values || !msgs_in || !msgs_out || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (pot->domain != SBP_SUM && pot->domain != SBP_MAX) return fail(SBP_EINVAL, "bad domain");
@@ -415,12 +440,14 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.err = err;
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
+        a.delta = delta;
         return cuda_status(fn(a, s), "sbp_iterate(band)");
     }
     if (pot->kind == SBP_POT_DENSE && pot->n_pot == 0 && pot->dense_t[0] && pot->dense_t[1] &&
         g->Ms >= 32) {
         if (pot->accumulate != SBP_ACC_F32)
             return fail(SBP_EUNSUPPORTED, "the dense kernel accumulates in f32");
+        if (delta) return fail(SBP_EUNSUPPORTED, "the dense kernel has no fused convergence test");
         sbp::DenseArgs a;
         a.values = values;
         a.msgs_in = msgs_in;
@@ -443,6 +470,7 @@ int sbp_iterate(const sbp_grid *g, const sbp_potential *pot, const float *values
         a.err = err;
         a.lr_begin = lr_begin; a.lr_end = lr_end; a.iteration = iteration;
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
+        a.delta = delta;
         return cuda_status(sbp::launch_ell(pot->domain, a, s), "sbp_iterate(ell)");
     }
     return fail(SBP_EINVAL, "unknown potential kind %d", pot->kind);
@@ -495,8 +523,22 @@ int sbp_iterate_fused(const sbp_grid *g, const sbp_potential *pot, const float *
     return cuda_status(fn(a, f, (cudaStream_t)stream), "sbp_iterate_fused");
 }
 
+static int sweep_impl(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                      float *msgs, int sweep, unsigned long long *err, float *delta, void *stream);
+
 int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, float *msgs,
               int sweep, unsigned long long *err, void *stream) {
+    return sweep_impl(g, pot, values, msgs, sweep, err, nullptr, stream);
+}
+
+int sbp_sweep_delta(const sbp_grid *g, const sbp_potential *pot, const float *values, float *msgs,
+                    int sweep, unsigned long long *err, float *delta, void *stream) {
+    if (!delta) return fail(SBP_EINVAL, "delta is NULL");
+    return sweep_impl(g, pot, values, msgs, sweep, err, delta, stream);
+}
+
+static int sweep_impl(const sbp_grid *g, const sbp_potential *pot, const float *values,
+                      float *msgs, int sweep, unsigned long long *err, float *delta, void *stream) {
     if (int rc = check_grid(g)) return rc;
     if (!pot || !values || !msgs || !err) return fail(SBP_EINVAL, "NULL pointer");
     if (g->r0 != 0 || g->rows != g->H) return fail(SBP_EINVAL, "sequential sweeps need the full grid");
@@ -510,6 +552,7 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
         a.msgs_out = msgs;
         a.err = err;
         a.lr_begin = 1; a.lr_end = g->H + 1; a.iteration = sweep;
+        a.delta = delta;
         return cuda_status(sbp::launch_ell_sweep(pot->domain, a, (cudaStream_t)stream),
                            "sbp_sweep(ell)");
     }
@@ -549,6 +592,7 @@ int sbp_sweep(const sbp_grid *g, const sbp_potential *pot, const float *values, 
         for (int d = -pot->R; d <= pot->R; ++d) a.w[o][d + Rk] = pot->band_w[o][d + pot->R];
     }
     sbp::band_pairs(a, Rk, pad);
+    a.delta = delta;
     return cuda_status(fn(a, (cudaStream_t)stream), "sbp_sweep");
 }
 
@@ -573,8 +617,10 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
             BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
             if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);
             if (ch.variant == 3)
-                snprintf(buf, len, "band_iter_tap_kernel<%s,VL=%d,LP=%d,R=%d%s%s>", dom, ch.vl,
-                         g->Ms / ch.vl, Rk, ch.rolled ? ",rolled" : "", ch.staged ? ",staged" : "");
+                snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s%s>",
+                         ch.staged == 2 ? "band_iter_tap2_kernel" : "band_iter_tap_kernel", dom,
+                         ch.vl, g->Ms / ch.vl, Rk, ch.rolled ? ",rolled" : "",
+                         ch.staged == 1 ? ",staged" : "");
             else
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
                          ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom,

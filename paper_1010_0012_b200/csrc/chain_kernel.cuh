@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__
     // and two other incoming vectors (independent of the chain) sit in a
     // register ring, loaded CHAIN_LA steps ahead; L2 prefetch CHAIN_PF ahead
     float chain[VL], gq[CHAIN_LA][VL], aq[CHAIN_LA][VL], bq[CHAIN_LA][VL];
+    float dmax = 0.0f;   // convergence test (BandArgs::delta): |new - old| in place
     Vec8Loader<VL>::load(chain, node_ptr(geo.wslot, src0));
     const long long len = geo.line_len;
 #pragma unroll
@@ -133,6 +134,9 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__
             bool ok;
             if (dir == 0 || dir == 2) ok = band_message<DOM, VL, LP, R, 0>(a, h, j, x0, chain);
             else ok = band_message<DOM, VL, LP, R, 1>(a, h, j, x0, chain);
+            if (a.delta && valid)
+                dmax = fmaxf(dmax, message_delta<DOM, VL>(chain, node_ptr(geo.wslot, src + geo.step),
+                                                          false, x0, a.M));
             if (valid) Vec8Loader<VL>::store(node_ptr(geo.wslot, src + geo.step), chain);
             if (!ok && valid && j == 0) {
                 // reference order of the first failure: sweep, pass, line, position
@@ -143,6 +147,7 @@ __global__ void __launch_bounds__(128) chain_pass_kernel(const __grid_constant__
             }
         }
     }
+    if (a.delta) flush_delta(a.delta, dmax);
 }
 
 template <int DOM, int VL, int LP, int R>

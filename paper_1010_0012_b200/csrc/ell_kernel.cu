@@ -192,6 +192,28 @@ __device__ __forceinline__ bool ell_message(const EllArgs &a, const float (&h)[E
     return isfinite(tot);
 }
 
+// max |out - old| over the lane's labels (old: the message being replaced;
+// iteration 0 of a synchronous run: the reference initial message)
+template <int DOM>
+__device__ __forceinline__ float ell_delta(const EllArgs &a, const float *old, int lane,
+                                          const float (&out)[ELL_QMAX], bool first) {
+    float d = 0.0f;
+#pragma unroll
+    for (int q = 0; q < ELL_QMAX; ++q) {
+        const int x = lane + 32 * q;
+        if (x < a.M) {
+            const float o = first ? (DOM == SBP_SUM ? 1.0f / (float)a.M : 0.0f) : old[x];
+            d = fmaxf(d, fabsf(out[q] - o));
+        }
+    }
+    return d;
+}
+
+__device__ __forceinline__ void ell_flush_delta(float *delta, float d) {
+    for (int off = 16; off; off >>= 1) d = fmaxf(d, __shfl_xor_sync(SBP_FULL_MASK, d, off));
+    if ((threadIdx.x & 31) == 0 && d > 0.0f) atomicMax(reinterpret_cast<int *>(delta), __float_as_int(d));
+}
+
 __device__ __forceinline__ void ell_store(const EllArgs &a, float *base, int lane,
                                           const float (&out)[ELL_QMAX]) {
 #pragma unroll
@@ -235,6 +257,7 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
     }
     const bool has[4] = {c + 1 < a.W, c > 0, r + 1 < a.H, r > 0};
     const long long W = a.W;
+    float dmax = 0.0f;
 #pragma unroll
     for (int dir = 0; dir < 4; ++dir) {
         if (!has[dir]) continue;
@@ -250,11 +273,13 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_iter_kernel(const __grid_c
             ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), out);
         }
         const long long step = dir == 0 ? 1 : dir == 1 ? -1 : dir == 2 ? W : -W;
-        ell_store(a, a.msgs_out + dir_wslot(dir) * a.slot_stride + (node_l + step) * a.Ms, lane,
-                  out);
+        const long long off = dir_wslot(dir) * a.slot_stride + (node_l + step) * a.Ms;
+        if (a.delta) dmax = fmaxf(dmax, ell_delta<DOM>(a, a.msgs_in + off, lane, out, a.first));
+        ell_store(a, a.msgs_out + off, lane, out);
         if (!ok && lane == 0)
             report_failure(a.err, a.iteration, directed_edge_id(a.H, W, r, c, dir));
     }
+    if (a.delta) ell_flush_delta(a.delta, dmax);
 }
 
 // Sequential (canonical) pass over chains, one warp per chain; see
@@ -278,6 +303,7 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_
     float *msgs = a.msgs_out;
     const long long S = a.slot_stride;
     long long src = line * stride + origin;
+    float dmax = 0.0f;
     float chain[ELL_QMAX];
 #pragma unroll
     for (int q = 0; q < ELL_QMAX; ++q) {
@@ -308,6 +334,9 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_
             ell_h<DOM>(g, m, excl, h);
             ok = ell_message<DOM>(a, h, hs, lane, ell_pot_slot(a, r, c, dir), chain);
         }
+        if (a.delta)
+            dmax = fmaxf(dmax, ell_delta<DOM>(a, msgs + wslot * S + (src + step + W) * a.Ms, lane,
+                                              chain, false));
         ell_store(a, msgs + wslot * S + (src + step + W) * a.Ms, lane, chain);
         if (!ok && lane == 0) {
             const unsigned long long key = ((unsigned long long)a.iteration << 40) |
@@ -317,6 +346,7 @@ __global__ void __launch_bounds__(32 * ELL_WARPS) ell_chain_kernel(const __grid_
         }
         __syncwarp();
     }
+    if (a.delta) ell_flush_delta(a.delta, dmax);
 }
 
 cudaError_t launch_ell(int domain, const EllArgs &a, cudaStream_t s) {

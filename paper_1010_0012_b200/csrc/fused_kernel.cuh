@@ -132,13 +132,10 @@ band_fused_kernel(const __grid_constant__ BandArgs a, const __grid_constant__ Fu
                     for (int i = 0; i < VL; ++i)
                         mm[q][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
                 }
-            } else if (l == 0) {
-                // messages of the previous launch: read-only during this one
-                Vec8Loader<VL>::load(m0, mi);
-                Vec8Loader<VL>::load(m1, mi + a.slot_stride);
-                Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
-                Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
             } else {
+                // level 0 reads the previous launch's messages, but level 2
+                // rewrites that buffer within this launch: no .nc (read-only
+                // for the kernel's lifetime) loads for messages at any level
                 Vec8LoaderCG<VL>::load(m0, mi);
                 Vec8LoaderCG<VL>::load(m1, mi + a.slot_stride);
                 Vec8LoaderCG<VL>::load(m2, mi + 2 * a.slot_stride);

@@ -166,6 +166,9 @@ __device__ __forceinline__ void tap_emit(const BandArgs &a, const IterCtx &it, c
     const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
     const long long dir_off = dir_wslot(DIR) * a.slot_stride + step * a.Ms;
     float *dst = it.msgs_out + (node_l * a.Ms + x0) + dir_off;
+    if (a.delta)
+        *it.dmax = fmaxf(*it.dmax, message_delta<DOM, VL>(out, it.msgs_in + (node_l * a.Ms + x0) + dir_off,
+                                                         it.first, x0, a.M));
     Vec8Loader<VL>::store(dst, out);
     if (!ok && j == 0) report_failure(a.err, it.iteration, directed_edge_id(a.H, W, r, c, DIR));
 }
@@ -279,7 +282,8 @@ band_iter_tap_kernel(const __grid_constant__ BandArgs a) {
     using SM = TapSmem<VL, LP, NS>;
     constexpr int PPW = 32 / LP;
     constexpr int VEC = 32 * VL;
-    const IterCtx it = iter_of(a);
+    float dmax = 0.0f;
+    const IterCtx it = iter_of(a, &dmax);
     extern __shared__ __align__(128) float tap_smem[];
     __shared__ __align__(8) unsigned long long bars[TAP_WARPS][2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -380,6 +384,7 @@ band_iter_tap_kernel(const __grid_constant__ BandArgs a) {
                                                r, c);
         if (NS == 2) st ^= 1;
     }
+    if (a.delta) flush_delta(a.delta, dmax);
 }
 
 template <int DOM, int VL, int LP, int R, bool ROLLED, int NS>
@@ -408,6 +413,318 @@ cudaError_t launch_band_tap(const BandArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// v2: register-light.  The four exclusion vectors of a node are formed once
+// (reference order, prefix-shared, error-free for max-sum) straight into four
+// shared-memory rows, so the input vectors die before the first band and no
+// h state crosses the direction loop: ~60 registers instead of 125-140, i.e.
+// 6-8 resident 4-warp blocks per SM instead of 3-4.  Each message then
+// streams its whole window (own labels and taps) from its row.
+// ---------------------------------------------------------------------------
+
+// Sum (S) or max (H) of a lane's h over the node, as band_message forms it.
+template <int DOM, int VL, int LP>
+__device__ __forceinline__ float node_reduce(const float (&h)[VL]) {
+    if (DOM == SBP_SUM) return lanes_sum<LP>(vsum(h));
+    float mx = fmaxf(h[0], h[1]);
+#pragma unroll
+    for (int i = 2; i < VL; i += 2) mx = fmax3(mx, h[i], h[i + 1]);
+    return lanes_max<LP>(mx);
+}
+
+template <int DOM, int VL, int LP>
+__device__ __forceinline__ void put_row(float *row, int x0, const float (&h)[VL]) {
+    using Row = TapRow<VL * LP>;
+#pragma unroll
+    for (int i = 0; i < VL; i += 4)
+        sts128(row + Row::phys(Row::PADL + x0 + i), h[i], h[i + 1], h[i + 2], h[i + 3]);
+}
+
+// One message from the node's row of direction `dir` (floor reduction `red`).
+template <int DOM, int VL, int LP, int R, int O>
+__device__ __forceinline__ bool tap2_message(const BandArgs &a, float red, int x0, const float *row,
+                                             float (&out)[VL]) {
+    using Row = TapRow<VL * LP>;
+    const float base = DOM == SBP_SUM ? (a.floor_term ? a.fbar[O] * red : 0.0f)
+                                      : (a.floor_term ? a.fbar[O] + red : -__builtin_huge_valf());
+#pragma unroll
+    for (int i = 0; i < VL; ++i) out[i] = base;
+#pragma unroll
+    for (int tc = -R; tc < VL + R; tc += 4) {
+        const float4 v = lds128(row + Row::phys(Row::PADL + x0 + tc));
+        const float hv[4] = {v.x, v.y, v.z, v.w};
+        if (DOM == SBP_SUM) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = tc + u;
+#pragma unroll
+                for (int i = 0; i < VL; i += 2) {
+                    const int d = t - i;
+                    if (d < -R || d > R + 1) continue;
+                    fma2(out[i], out[i + 1], a.wp[O][d + R + 1], hv[u]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u += 2) {
+                const int t = tc + u;
+#pragma unroll
+                for (int i = 0; i < VL; i += 2) {
+                    const int d0 = t - i, d1 = t + 1 - i;
+                    const bool in0 = d0 >= -R && d0 <= R + 1;
+                    const bool in1 = d1 >= -R && d1 <= R + 1;
+                    float a0, a1, b0, b1;
+                    if (in0) add2(a0, a1, a.wp[O][d0 + R + 1].x, a.wp[O][d0 + R + 1].y, hv[u], hv[u]);
+                    if (in1) add2(b0, b1, a.wp[O][d1 + R + 1].x, a.wp[O][d1 + R + 1].y, hv[u + 1], hv[u + 1]);
+                    if (in0 && in1) {
+                        out[i] = fmax3(out[i], a0, b0);
+                        out[i + 1] = fmax3(out[i + 1], a1, b1);
+                    } else if (in0) {
+                        out[i] = fmaxf(out[i], a0);
+                        out[i + 1] = fmaxf(out[i + 1], a1);
+                    } else if (in1) {
+                        out[i] = fmaxf(out[i], b0);
+                        out[i + 1] = fmaxf(out[i + 1], b1);
+                    }
+                }
+            }
+        }
+    }
+    bool ok;
+    if (DOM == SBP_SUM) {
+        if (a.M < a.Ms) {
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                if (x0 + i >= a.M) out[i] = 0.0f;
+        }
+        const float s = lanes_sum<LP>(vsum(out));
+        ok = (s > 0.0f) && !isinf(s);
+        const float inv = __frcp_rn(s);
+#pragma unroll
+        for (int i = 0; i < VL; i += 2) mul2(out[i], out[i + 1], out[i], out[i + 1], inv, inv);
+    } else {
+        if (a.M < a.Ms) {
+#pragma unroll
+            for (int i = 0; i < VL; ++i)
+                if (x0 + i >= a.M) out[i] = -__builtin_huge_valf();
+        }
+        float mx = fmaxf(out[0], out[1]);
+#pragma unroll
+        for (int i = 2; i < VL; i += 2) mx = fmax3(mx, out[i], out[i + 1]);
+        mx = lanes_max<LP>(mx);
+        ok = isfinite(mx);
+#pragma unroll
+        for (int i = 0; i < VL; i += 2) sub2(out[i], out[i + 1], out[i], out[i + 1], mx, mx);
+    }
+    return ok;
+}
+
+template <int DOM, int VL, int LP, int R, int O>
+__device__ __forceinline__ void tap2_emit(const BandArgs &a, const IterCtx &it, float red,
+                                          const float *row, int DIR, int j, int x0, bool active,
+                                          long long node_l, long long r, int c) {
+    float out[VL];
+    const bool ok = tap2_message<DOM, VL, LP, R, O>(a, red, x0, row, out);
+    if (!active) return;
+    const long long W = a.W;
+    const long long step = DIR == 0 ? 1 : DIR == 1 ? -1 : DIR == 2 ? W : -W;
+    const long long dir_off = dir_wslot(DIR) * a.slot_stride + step * a.Ms;
+    float *dst = it.msgs_out + (node_l * a.Ms + x0) + dir_off;
+    if (a.delta)
+        *it.dmax = fmaxf(*it.dmax, message_delta<DOM, VL>(out, it.msgs_in + (node_l * a.Ms + x0) + dir_off,
+                                                         it.first, x0, a.M));
+    Vec8Loader<VL>::store(dst, out);
+    if (!ok && j == 0) report_failure(a.err, it.iteration, directed_edge_id(a.H, W, r, c, DIR));
+}
+
+// Rows of a node: rows[dir] holds h_{i \ dir's target}; red[dir] its S / H.
+template <int DOM, int VL, int LP>
+__device__ __forceinline__ void tap2_form_h(const float (&g)[VL], const float (&m0)[VL],
+                                            const float (&m1)[VL], const float (&m2)[VL],
+                                            const float (&m3)[VL], int x0, float *rows,
+                                            float (&red)[4]) {
+    constexpr int ROWF = TapRow<VL * LP>::PHYS;
+    float h[VL];
+    if (DOM == SBP_SUM) {
+        // reference order: unary, slots 0..3 ascending skipping the excluded
+        // one; the same association as band_group_body (bitwise equal)
+        vmul(h, g, m1);
+        vmul(h, h, m2);
+        vmul(h, h, m3);                               // excl 0 -> dir 3
+        put_row<DOM, VL, LP>(rows + 3 * ROWF, x0, h);
+        red[3] = node_reduce<DOM, VL, LP>(h);
+        float ab[VL];
+        vmul(ab, g, m0);
+        vmul(h, ab, m2);
+        vmul(h, h, m3);                               // excl 1 -> dir 1
+        put_row<DOM, VL, LP>(rows + 1 * ROWF, x0, h);
+        red[1] = node_reduce<DOM, VL, LP>(h);
+        vmul(ab, ab, m1);
+        vmul(h, ab, m3);                              // excl 2 -> dir 0
+        put_row<DOM, VL, LP>(rows + 0 * ROWF, x0, h);
+        red[0] = node_reduce<DOM, VL, LP>(h);
+        vmul(h, ab, m2);                              // excl 3 -> dir 2
+        put_row<DOM, VL, LP>(rows + 2 * ROWF, x0, h);
+        red[2] = node_reduce<DOM, VL, LP>(h);
+    } else {
+        float s2[VL], e2[VL];
+        vtwo_sum(g, m1, s2, e2);
+        vtwo_sum_acc(s2, m2, e2, e2);
+        vtwo_sum_acc(s2, m3, e2, e2);
+        shift_compensated<VL, LP>(s2, e2, h);        // excl 0 -> dir 3
+        put_row<DOM, VL, LP>(rows + 3 * ROWF, x0, h);
+        red[3] = node_reduce<DOM, VL, LP>(h);
+        float sa[VL], ea[VL];
+        vtwo_sum(g, m0, sa, ea);
+        vtwo_sum_from(sa, ea, m2, s2, e2);
+        vtwo_sum_acc(s2, m3, e2, e2);
+        shift_compensated<VL, LP>(s2, e2, h);        // excl 1 -> dir 1
+        put_row<DOM, VL, LP>(rows + 1 * ROWF, x0, h);
+        red[1] = node_reduce<DOM, VL, LP>(h);
+        vtwo_sum_acc(sa, m1, ea, ea);
+        vtwo_sum_from(sa, ea, m3, s2, e2);
+        shift_compensated<VL, LP>(s2, e2, h);        // excl 2 -> dir 0
+        put_row<DOM, VL, LP>(rows + 0 * ROWF, x0, h);
+        red[0] = node_reduce<DOM, VL, LP>(h);
+        vtwo_sum_from(sa, ea, m2, s2, e2);
+        shift_compensated<VL, LP>(s2, e2, h);        // excl 3 -> dir 2
+        put_row<DOM, VL, LP>(rows + 2 * ROWF, x0, h);
+        red[2] = node_reduce<DOM, VL, LP>(h);
+    }
+}
+
+template <int VL, int LP>
+struct Tap2Smem {
+    static constexpr int PPW = 32 / LP;
+    static constexpr int ROWF = TapRow<VL * LP>::PHYS;
+    static constexpr int WARP_F = (PPW * 4 * ROWF + 31) / 32 * 32;
+    static constexpr size_t bytes() { return (size_t)TAP_WARPS * WARP_F * sizeof(float); }
+};
+
+template <int DOM, int VL, int LP>
+__device__ __forceinline__ void tap2_rows_init(float *wbase) {
+    using Row = TapRow<VL * LP>;
+    constexpr int NROWS = 4 * (32 / LP);
+    constexpr float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
+    const int lane = threadIdx.x & 31;
+    constexpr int PER = 2 * Row::PADL / 4;   // 4-float pad chunks per row
+    for (int k = lane; k < NROWS * PER; k += 32) {
+        const int rw = k / PER, q = k % PER;
+        const int y = q < Row::PADL / 4 ? 4 * q : Row::PADL + VL * LP + 4 * (q - Row::PADL / 4);
+        sts128(wbase + rw * Row::PHYS + Row::phys(y), PAD, PAD, PAD, PAD);
+    }
+    __syncwarp();
+}
+
+#ifndef SBP_TAP2_BLOCKS
+#define SBP_TAP2_BLOCKS 8
+#endif
+template <int DOM, int VL, int LP, int R, bool ROLLED>
+__global__ void __launch_bounds__(32 * TAP_WARPS, (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6))
+band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
+    using SM = Tap2Smem<VL, LP>;
+    constexpr int PPW = 32 / LP;
+    constexpr int ROWF = SM::ROWF;
+    float dmax = 0.0f;
+    const IterCtx it = iter_of(a, &dmax);
+    extern __shared__ __align__(128) float tap_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = lane % LP, q = lane / LP;
+    const int x0 = j * VL;
+    float *wbase = tap_smem + warp * SM::WARP_F;
+    float *rows = wbase + q * 4 * ROWF;
+    tap2_rows_init<DOM, VL, LP>(wbase);
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long ngroups = (npix + PPW - 1) / PPW;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; grp < ngroups;
+         grp += nwarps) {
+        long long p = grp * PPW + q;
+        const bool valid = p < npix;
+        if (!valid) p = npix - 1;
+        const int lr = it.lr_begin + (int)(p / a.W);
+        const int c = (int)(p % a.W);
+        const long long r = (long long)a.r0 + lr - 1;
+        const long long node_l = (long long)lr * a.W + c;
+        float red[4];
+        {
+            float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
+            Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
+            if (!it.first) {
+                const float *mi = it.msgs_in + node_l * a.Ms + x0;
+                Vec8Loader<VL>::load(m0, mi);
+                Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+                Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+                Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+            } else {
+                const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+                float *mm[4] = {m0, m1, m2, m3};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float real = DOM == SBP_SUM ? (ghost[k] ? 1.0f : 1.0f / (float)a.M) : 0.0f;
+#pragma unroll
+                    for (int i = 0; i < VL; ++i)
+                        mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
+                }
+            }
+            __syncwarp();   // the previous node's messages are done reading the rows
+            tap2_form_h<DOM, VL, LP>(g, m0, m1, m2, m3, x0, rows, red);
+        }
+        __syncwarp();
+        const unsigned has = (c + 1 < a.W ? 1u : 0u) | (c > 0 ? 2u : 0u) |
+                             (r + 1 < a.H ? 4u : 0u) | (r > 0 ? 8u : 0u);
+        auto one = [&](int dir, float rd) {
+            const bool hd = (has >> dir) & 1u;
+            if (!__any_sync(SBP_FULL_MASK, valid && hd)) return;
+            if (ROLLED || dir == 0 || dir == 2)
+                tap2_emit<DOM, VL, LP, R, 0>(a, it, rd, rows + dir * ROWF, dir, j, x0, valid && hd,
+                                             node_l, r, c);
+            else
+                tap2_emit<DOM, VL, LP, R, 1>(a, it, rd, rows + dir * ROWF, dir, j, x0, valid && hd,
+                                             node_l, r, c);
+        };
+        if constexpr (ROLLED) {
+#pragma unroll 1
+            for (int k = 0; k < 4; ++k) {
+                const int dir = (0x2013 >> (4 * k)) & 0xF;   // order 3, 1, 0, 2
+                const float rd = dir == 0 ? red[0] : dir == 1 ? red[1] : dir == 2 ? red[2] : red[3];
+                one(dir, rd);
+            }
+        } else {
+            one(3, red[3]);
+            one(1, red[1]);
+            one(0, red[0]);
+            one(2, red[2]);
+        }
+    }
+    if (a.delta) flush_delta(a.delta, dmax);
+}
+
+template <int DOM, int VL, int LP, int R, bool ROLLED>
+cudaError_t launch_band_tap2(const BandArgs &a, cudaStream_t s) {
+    constexpr int PPW = 32 / LP;
+    const size_t smem = Tap2Smem<VL, LP>::bytes();
+    static int resident = 0, sms = 0;
+    if (!resident) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &resident, band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED>, 32 * TAP_WARPS, smem);
+        if (resident < 1) resident = 1;
+    }
+    const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    const long long warps = (npix + PPW - 1) / PPW;
+    long long blocks = (warps + TAP_WARPS - 1) / TAP_WARPS;
+    if (blocks <= 0) return cudaSuccess;
+    const long long cap = (long long)sms * resident;
+    if (blocks > cap) blocks = cap;
+    band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED><<<(unsigned)blocks, 32 * TAP_WARPS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 // Radii with a shared-memory-tap kernel (multiples of 4: 4-tap chunks).
 // variant: 0 register-loaded, 1 TMA-staged (2 stages), rolled or unrolled.
 template <int MS, int DOM>
@@ -417,6 +734,9 @@ BandLaunchFn pick_band_tap(int vl, int R, bool rolled, int staged) {
     } else {
 #define SBP_TAP(RR)                                                                          \
     if (R == RR) {                                                                           \
+        if (vl == 8 && staged == 2)                                                          \
+            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true>                      \
+                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false>;                    \
         if (vl == 8) {                                                                       \
             if (rolled) return staged ? &launch_band_tap<DOM, 8, MS / 8, RR, true, 2>        \
                                       : &launch_band_tap<DOM, 8, MS / 8, RR, true, 0>;       \

@@ -183,7 +183,8 @@ class GridEngine:
 
     def __init__(self, model, domain: str = "sum", kernel: str = "fast", device=None,
                  r0: int = 0, rows: int | None = None, values: np.ndarray | None = None,
-                 schedule: str = SYNCHRONOUS, precision: str | None = None):
+                 schedule: str = SYNCHRONOUS, precision: str | None = None,
+                 defer_values: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("the GPU grid engine needs a CUDA device (no CPU fallback)")
         self.lib = L.lib()
@@ -231,7 +232,8 @@ class GridEngine:
             self.err = torch.full((1,), -1, dtype=torch.int64, device=self.device)
             self.values = torch.empty((self.rows, self.W, self.Ms), dtype=torch.float32,
                                       device=self.device)
-            self.upload_values(values)
+            if not defer_values:         # else run_streamed uploads them by row bands
+                self.upload_values(values)
         for buf in self.msgs:
             self._init(buf, ghosts_only=True)
         # temporal blocking (sbp_iterate_fused): up to `fuse` synchronous
@@ -324,6 +326,81 @@ class GridEngine:
                                          _ptr(self.values), _stream_handle(self.device)))
         self._staging = dev   # keep alive until the stream consumed it
 
+    def run_streamed(self, iters: int, values=None, bands: int = 8,
+                     events: list | None = None) -> None:
+        """``iters`` synchronous iterations from the reference initial messages,
+        overlapped with the host->device upload of the f64 unary table.
+
+        The table crosses PCIe in ``bands`` row bands on a copy stream (pinned
+        host memory makes the copies asynchronous) and each band is converted
+        to the padded f32 layout as it lands.  Iterations run as a row
+        wavefront: iteration t covers the rows whose inputs exist, its
+        frontier trailing iteration t-1's by one row (a row needs the
+        previous iteration's messages from the row below).  Because
+        iteration t+1 only ever writes rows that iteration t has finished,
+        the ping-pong buffers stay race-free, and the arithmetic is that of
+        ``step``: bit-identical results."""
+        if self.plan is None or self.r0 != 0 or self.rows != self.H:
+            raise NotImplementedError("streamed upload runs a whole single-GPU grid")
+        H, W = self.H, self.W
+        if values is None:
+            values = self.model.unaries if self.domain == "sum" else self.model.log_unaries
+        arr = np.ascontiguousarray(values, dtype=np.float64)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.from_numpy(arr)
+        pinned = host.is_pinned()
+        cs = torch.cuda.current_stream(self.device)
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=self.device)
+        copy = self._copy_stream
+        copy.wait_stream(cs)
+        bands = max(1, min(bands, H))
+        step = -(-H // bands)
+        frontier = [0] * iters
+        self.err.fill_(-1)
+        keep = []
+        for b0 in range(0, H, step):
+            nb = min(step, H - b0)
+            ev = torch.cuda.Event()
+            with torch.cuda.stream(copy):
+                chunk = host[b0 * W:(b0 + nb) * W].to(self.device, non_blocking=pinned)
+                ev.record(copy)
+            cs.wait_event(ev)
+            chunk.record_stream(cs)
+            keep.append(chunk)
+            g = L.SbpGrid(H, W, self.M, self.Ms, b0, nb, self.device.index)
+            L.check(self.lib.sbp_load_values(ctypes_ref(g), self.dom, _ptr(chunk),
+                                             _ptr(self.values) + b0 * W * self.Ms * 4,
+                                             _stream_handle(self.device)))
+            ready = b0 + nb
+            for t in range(iters):
+                if t == 0:
+                    new = ready
+                else:
+                    new = frontier[t - 1] if frontier[t - 1] == H else frontier[t - 1] - 1
+                if new <= frontier[t]:
+                    break           # iteration t is stuck, so is every later one
+                ev0 = None
+                if events is not None:
+                    ev0 = torch.cuda.Event(enable_timing=True)
+                    ev0.record(cs)
+                L.check(self.lib.sbp_iterate(
+                    ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
+                    _ptr(self.msgs[t % 2]), _ptr(self.msgs[(t + 1) % 2]), frontier[t] + 1,
+                    new + 1, t, L.SBP_ITER_FIRST if t == 0 else 0, _ptr(self.err),
+                    _stream_handle(self.device)))
+                if events is not None:
+                    ev1 = torch.cuda.Event(enable_timing=True)
+                    ev1.record(cs)
+                    events.append((ev0, ev1, (new - frontier[t]) / H))
+                frontier[t] = new
+        assert all(f == H for f in frontier)
+        self._staging = keep
+        self.cur = iters % 2
+        self.iterations = iters
+        self._init_valid = True
+
     @property
     def kernel_name(self) -> str:
         """The kernel instantiation this engine launches per iteration / sweep."""
@@ -367,16 +444,31 @@ class GridEngine:
             self._init_valid = True
         return self.msgs[self.cur]
 
-    def iterate_rows(self, lr_begin: int, lr_end: int, stream: int | None = None) -> None:
+    def iterate_rows(self, lr_begin: int, lr_end: int, stream: int | None = None,
+                     delta: torch.Tensor | None = None) -> None:
         """One synchronous iteration over local rows [lr_begin, lr_end) from the
-        current buffer into the other one (does not flip buffers)."""
+        current buffer into the other one (does not flip buffers).  ``delta``
+        (device float32 scalar): fused convergence test, max |new - old|."""
         if self.plan is None:
             return
-        L.check(self.lib.sbp_iterate(
-            ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
-            _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), lr_begin, lr_end,
-            self.iterations, L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self.err),
-            _stream_handle(self.device) if stream is None else stream))
+        args = (ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
+                _ptr(self.msgs[self.cur]), _ptr(self.msgs[1 - self.cur]), lr_begin, lr_end,
+                self.iterations, L.SBP_ITER_FIRST if self.iterations == 0 else 0, _ptr(self.err))
+        s = _stream_handle(self.device) if stream is None else stream
+        if delta is None:
+            L.check(self.lib.sbp_iterate(*args, s))
+        else:
+            L.check(self.lib.sbp_iterate_delta(*args, _ptr(delta), s))
+
+    @property
+    def fused_delta(self) -> bool:
+        """Whether the convergence test can ride in the iteration kernels
+        (all but the tiled dense comparison kernel of the synchronous schedule)."""
+        if self.plan is None:
+            return False
+        tiled_dense = (self.plan.kind == L.SBP_POT_DENSE and self.Ms >= 32
+                       and not self.plan.n_pot)
+        return self.schedule == SEQUENTIAL or not tiled_dense
 
     def flip(self) -> None:
         self.cur = 1 - self.cur
@@ -411,26 +503,32 @@ class GridEngine:
         self.iterations += levels
         return True
 
-    def sweep(self) -> None:
+    def sweep(self, delta: torch.Tensor | None = None) -> None:
         """One canonical sequential sweep in place (reference ``_run_grid``)."""
         if self.plan is not None:
-            L.check(self.lib.sbp_sweep(ctypes_ref(self.grid), ctypes_ref(self._pot_struct),
-                                       _ptr(self.values), _ptr(self.msgs[0]), self.iterations,
-                                       _ptr(self.err), _stream_handle(self.device)))
+            args = (ctypes_ref(self.grid), ctypes_ref(self._pot_struct), _ptr(self.values),
+                    _ptr(self.msgs[0]), self.iterations, _ptr(self.err))
+            if delta is None:
+                L.check(self.lib.sbp_sweep(*args, _stream_handle(self.device)))
+            else:
+                L.check(self.lib.sbp_sweep_delta(*args, _ptr(delta), _stream_handle(self.device)))
         self.iterations += 1
 
     def snapshot(self) -> None:
         """Keep a copy of the current messages (sequential convergence test)."""
         self.msgs[1].copy_(self.msgs[0])
 
-    def step(self, n: int = 1, events: list | None = None) -> None:
+    def step(self, n: int = 1, events: list | None = None,
+             delta: torch.Tensor | None = None) -> None:
+        """``n`` iterations (sweeps); ``delta``: fused convergence test of the
+        last one (device float32 scalar, max-updated, zeroed by the caller)."""
         if self.schedule == SEQUENTIAL:
             for _ in range(n):
                 ev0 = ev1 = None
                 if events is not None:
                     ev0 = torch.cuda.Event(enable_timing=True)
                     ev0.record(torch.cuda.current_stream(self.device))
-                self.sweep()
+                self.sweep(delta)
                 if events is not None:
                     ev1 = torch.cuda.Event(enable_timing=True)
                     ev1.record(torch.cuda.current_stream(self.device))
@@ -438,13 +536,13 @@ class GridEngine:
             return
         done = 0
         while done < n:
-            k = min(self.fuse, n - done) if self._can_fuse() else 1
+            k = min(self.fuse, n - done) if (self._can_fuse() and delta is None) else 1
             if events is not None:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record(torch.cuda.current_stream(self.device))
             if k < 2 or not self.iterate_fused(k):
                 k = 1
-                self.iterate_rows(1, self.rows + 1)
+                self.iterate_rows(1, self.rows + 1, delta=delta)
                 self.flip()
             if events is not None:
                 ev1 = torch.cuda.Event(enable_timing=True)
@@ -635,6 +733,9 @@ class MessageStore:
             assert (self.data.max(axis=1) == 0.0).all(), "max-domain message max is not exactly 0"
 
 
+STREAM_MIN_BYTES = 64 << 20   # smaller unary tables upload in one piece
+
+
 def _schedule_mode(schedule) -> str:
     """None / the reference canonical SweepSchedule -> sequential (bp.py:647-648);
     "synchronous" -> Jacobi."""
@@ -672,25 +773,56 @@ def run_sweeps(model, n_sweeps: int, kernel: str = "fast", domain: str = "sum",
         store = MessageStore(model, domain, engine=None)
         store.stats = stats
         return store
+    # host unary tables (not built on the device from an image pair) of a
+    # single-GPU synchronous run stream in by row bands under the first
+    # iterations instead of crossing PCIe before iteration 0
+    streamed = (engine is None and mode == SYNCHRONOUS and convergence_tol is None
+                and getattr(model, "stereo_source", None) is None
+                and int(model.n_nodes) * int(model.M) * 8 >= STREAM_MIN_BYTES
+                and os.environ.get("SBP_STREAM", "1") != "0")
     eng = engine if engine is not None else GridEngine(model, domain, kernel, device=device,
-                                                       schedule=mode, precision=precision)
+                                                       schedule=mode, precision=precision,
+                                                       defer_values=streamed)
+    if streamed and (eng.plan is None or eng._can_fuse()):
+        eng.upload_values()         # the temporally blocked kernel runs whole grids
+        streamed = False
     if engine is not None or convergence_tol is not None:
-        eng.reset(full=convergence_tol is not None)
+        eng.reset(full=convergence_tol is not None and not eng.fused_delta)
     per_iter = 2 * int(model.n_edges)
     events: list = []
-    if convergence_tol is None:
+    if streamed:
+        cs = torch.cuda.current_stream(eng.device)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(cs)
+        eng.run_streamed(n_sweeps)
+        ev1.record(cs)
+        events.append((ev0, ev1, n_sweeps))   # includes the overlapped upload
+        stats.sweeps_run += n_sweeps
+        stats.n_updates += per_iter * n_sweeps
+    elif convergence_tol is None:
         # no per-sweep test: the engine may fuse iterations into one launch
         eng.step(n_sweeps, events=events)
         stats.sweeps_run += n_sweeps
         stats.n_updates += per_iter * n_sweeps
     else:
+        # fused: the iteration kernels compare each message with the one it
+        # replaces (no snapshot, no second pass); the tiled dense kernel keeps
+        # the separate max |a - b| pass
+        fused = eng.fused_delta
+        delta = torch.zeros(1, dtype=torch.float32, device=eng.device)
         for _ in range(n_sweeps):
-            if mode == SEQUENTIAL:
-                eng.snapshot()
-            eng.step(1, events=events)
+            if fused:
+                delta.zero_()
+                eng.step(1, events=events, delta=delta)
+                d = float(delta.item())
+            else:
+                if mode == SEQUENTIAL:
+                    eng.snapshot()
+                eng.step(1, events=events)
+                d = eng.max_abs_delta()
             stats.sweeps_run += 1
             stats.n_updates += per_iter
-            if eng.max_abs_delta() < convergence_tol:
+            if d < convergence_tol:
                 stats.converged = True
                 break
     torch.cuda.synchronize(eng.device)

@@ -112,7 +112,7 @@ def test_weak_smoothing_wide_band_f64_accumulation(schedule):
         ref_store = oracle.store_data(model, ref)
         rb, _ = oracle.beliefs(model, ref)
     else:
-        ref = oracle.seq_run(model, 20, "sum", "fast")
+        ref, _ = oracle.seq_run(model, 20, "sum", "fast")
         ref_store = oracle.store_data(model, ref)
         rb, _ = oracle.beliefs(model, ref)
     dev = oracle.rel_deviation(store.data, ref_store, floor=1e-30)

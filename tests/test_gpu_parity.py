@@ -434,3 +434,64 @@ def test_tap_and_shuffle_kernels_agree_bitwise(tmp_path, name, domain, variant):
     b = _run_subprocess({"SBP_TAP": "0", "SBP_BAND_VL": "8", "SBP_STAGED": "0",
                          "SBP_ROLL_MIN_R": "99"}, name, domain, 7, tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("schedule", ["synchronous", "sequential"])
+@pytest.mark.parametrize("domain", ["sum", "max"])
+@pytest.mark.parametrize("pot_kind", ["band", "ell"])
+def test_fused_convergence_delta_is_exact(schedule, domain, pot_kind):
+    """The fused convergence test (sbp_iterate_delta / sbp_sweep_delta) equals
+    max |new - old| over every message slot, computed explicitly."""
+    from paper_1010_0012_b200.engine import GridEngine
+    model = synth.build_config_model(synth.CONFIGS["C2"], height=30, width=44)
+    if pot_kind == "ell":   # a non-Toeplitz potential plans as ELL
+        d = model.shared_potential.densify().table.copy()
+        d[3, 5] *= 0.5
+        model = sbp.GridMrf(30, 44, model.M, model.unaries,
+                            sbp.sparse_from_dense(d, fbar=model.shared_potential.fbar),
+                            log_unaries=model.log_unaries)
+    eng = GridEngine(model, domain, "fast", schedule=schedule)
+    assert eng.fused_delta and eng.plan.kind_name == pot_kind
+    eng.reset(full=True)
+    delta = torch.zeros(1, dtype=torch.float32, device=eng.device)
+    M = model.M
+    for _ in range(4):
+        prev = eng.current[:, :, :, :M].clone()
+        delta.zero_()
+        eng.step(1, delta=delta)
+        diff = (eng.current[:, :, :, :M] - prev).abs()
+        want = float(torch.nan_to_num(diff, nan=0.0).max())
+        assert float(delta.item()) == want
+
+
+def test_convergence_tol_sequential_matches_oracle():
+    model = synth.build_config_model(synth.CONFIGS["C1"], height=16, width=20)
+    tol = 1e-4
+    store = sbp.run_sweeps(model, 100, convergence_tol=tol)      # reference default schedule
+    assert store.stats.converged
+    n = store.stats.sweeps_run
+    # the reference's rule: the first sweep whose max change is below tol
+    a, _ = oracle.seq_run(model, n - 1, "sum", "fast")
+    b, _ = oracle.seq_run(model, n, "sum", "fast")
+    assert np.abs(b - a).max() < tol * 1.01
+    if n > 2:
+        c, _ = oracle.seq_run(model, n - 2, "sum", "fast")
+        assert np.abs(a - c).max() >= tol * 0.99
+
+
+@pytest.mark.parametrize("domain", ["sum", "max"])
+def test_streamed_upload_wavefront_is_bitwise(monkeypatch, domain):
+    """Host unaries streamed in row bands under a row wavefront of iterations
+    (GridEngine.run_streamed) give the same bits as upload-then-iterate."""
+    from paper_1010_0012_b200 import engine as E
+    model = synth.build_config_model(synth.CONFIGS["C2"], height=61, width=47)
+    monkeypatch.setenv("SBP_STREAM", "0")
+    want = sbp.run_sweeps(model, 23, domain=domain, schedule=SYNC).engine.msgs4()
+    monkeypatch.setenv("SBP_STREAM", "1")
+    monkeypatch.setattr(E, "STREAM_MIN_BYTES", 0)
+    for bands in (1, 3, 8, 61):
+        eng = E.GridEngine(model, domain, "fast", defer_values=True)
+        eng.run_streamed(23, bands=bands)
+        np.testing.assert_array_equal(eng.msgs4(), want)
+    store = sbp.run_sweeps(model, 23, domain=domain, schedule=SYNC)
+    np.testing.assert_array_equal(store.engine.msgs4(), want)
