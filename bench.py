@@ -319,6 +319,8 @@ def run_ours(args, cfg):
         eng = GridEngine(smodel, args.domain, "fast", device=dev, values=values)
     torch.cuda.synchronize()
     iter_events: list = []
+    strip_timing: list = []
+    host_s: list = []
 
     def step(record):
         eng.reset()
@@ -326,7 +328,11 @@ def run_ours(args, cfg):
             if record:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
-            run_rank(strip, args.iters, rank, world, interior_stream=interior)
+            strip_timing.clear()
+            h0 = time.perf_counter()
+            run_rank(strip, args.iters, rank, world, interior_stream=interior,
+                     timing=strip_timing if record else None)
+            host_s.append(time.perf_counter() - h0)
             if record:
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev1.record()
@@ -362,6 +368,15 @@ def run_ours(args, cfg):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    per_rank = None
+    if world > 1:
+        from paper_1010_0012_b200.strips import summarize_timing
+        mine = summarize_timing(strip_timing)      # last timed step, medians
+        mine.update(rank=rank, rows=rows,
+                    host_enqueue_ms_per_iteration=float(np.median(host_s)) / args.iters * 1e3)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        per_rank = gathered
     # message-kernel launches: (ms, iterations in the launch).  A fused launch
     # (temporal blocking) runs `levels` iterations and moves the algorithmic
     # bytes B once; the roofline is taken over the full-length launches.
@@ -423,6 +438,7 @@ def run_ours(args, cfg):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks.summary(),
         "configs": others,
+        "per_rank": per_rank,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -832,6 +832,7 @@ cudaError_t launch_band_staged(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
+    if (launch_block_cap() > 0 && blocks > launch_block_cap()) blocks = launch_block_cap();
     band_iter_staged_kernel<DOM, VL, LP, R, NS><<<(unsigned)blocks, 32 * STG_WARPS, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -885,6 +886,7 @@ cudaError_t launch_band(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
+    if (launch_block_cap() > 0 && blocks > launch_block_cap()) blocks = launch_block_cap();
     band_iter_kernel<DOM, VL, LP, R, ROLLED><<<(unsigned)blocks, 128, 0, s>>>(a);
     return cudaGetLastError();
 }

@@ -113,6 +113,7 @@ struct EnvKnobs {
     int tap_vl = env_int_raw("SBP_TAP_VL", 0);
     int tap_staged = env_int_raw("SBP_TAP_STAGED", -1);
     int tap_rolled = env_int_raw("SBP_TAP_ROLLED", -1);
+    int max_blocks = env_int_raw("SBP_MAX_BLOCKS", 0);
 };
 EnvKnobs &knobs() {
     static EnvKnobs k;
@@ -149,7 +150,8 @@ bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     if (k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = k.tap_vl;
     c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym) : (sym && Rk >= 32);
     // staged: 0 register-loaded inputs, 1 TMA-staged inputs, 2 register-light
-    // v2 (all four exclusion vectors in shared-memory rows); VL = 8 only
+    // v2 (all four exclusion vectors in shared-memory rows), 3 v2 with the next
+    // group's inputs TMA-prefetched; 1..3 need VL = 8
     c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0)
                                  : (domain == SBP_MAX && c.vl == 8 ? 1 : 0);
     return true;
@@ -330,6 +332,10 @@ int ell_args(const sbp_grid *g, const sbp_potential *pot, sbp::EllArgs *a) {
 }
 
 }  // namespace
+
+namespace sbp {
+int launch_block_cap() { return knobs().max_blocks; }
+}
 
 extern "C" {
 
@@ -618,9 +624,9 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
             if (Rk) band_resolve(g->Ms, pot->domain, Rk, ch);
             if (ch.variant == 3)
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s%s>",
-                         ch.staged == 2 ? "band_iter_tap2_kernel" : "band_iter_tap_kernel", dom,
+                         ch.staged >= 2 ? "band_iter_tap2_kernel" : "band_iter_tap_kernel", dom,
                          ch.vl, g->Ms / ch.vl, Rk, ch.rolled ? ",rolled" : "",
-                         ch.staged == 1 ? ",staged" : "");
+                         (ch.staged == 1 || ch.staged == 3) ? ",staged" : "");
             else
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
                          ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom,

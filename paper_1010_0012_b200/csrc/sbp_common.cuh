@@ -10,6 +10,11 @@
 
 namespace sbp {
 
+// Upper bound on the blocks of a persistent (grid-stride) launch: 0 = no cap
+// beyond residency.  SBP_MAX_BLOCKS (read once, sbp_reload_config) changes the
+// launch geometry for race checks (tests/test_gpu_guards.py).  Defined in capi.cu.
+int launch_block_cap();
+
 // Reference directed-edge id (bp.py:113-133 over the edge order of
 // mrf.py:401-411): node-major, each node emits (n, n+1) then (n, n+W);
 // undirected edge e yields 2e for a->b and 2e+1 for b->a.

@@ -19,22 +19,31 @@
 //   (0 / -inf) on both sides, written once per launch, so no selects are
 //   needed, and taps never occupy more than one 4-float chunk of registers.
 //
-// Rows use a skewed layout (4 floats of padding after every 32) so the
-// 8 lanes of each LDS.128 / STS.128 phase hit 8 distinct 16-byte bank groups
-// for every lane stride used here (VL = 8 and 16): conflict-free.
+// Rows use an XOR-swizzled layout (TapRow) so the 8 lanes of each LDS.128 /
+// STS.128 phase hit 8 distinct 16-byte bank groups for both lane strides
+// used here (VL = 8 and 16): conflict-free.
 #pragma once
 
 #include "band_kernel.cuh"
 
 namespace sbp {
 
-template <int MS>
+// Row of one node's h in shared memory: PADL pad labels, Ms labels, PADL pad
+// labels.  16-byte chunks are XOR-swizzled within each 128-byte line group so
+// that the 8 lanes of an LDS.128 / STS.128 phase, which touch chunks
+// c, c + VL/4, ..., c + 7 VL/4 (lane stride VL labels), land in 8 distinct
+// bank groups for every c: chunk k lives at k ^ ((k >> 3) & (VL/4 - 1)).
+template <int MS, int VL>
 struct TapRow {
     static constexpr int PADL = 32;                  // >= SBP_MAX_R, multiple of 32
-    static constexpr int L = MS + 2 * PADL;          // logical floats
-    static constexpr int PHYS = L + L / 8;           // + 4 floats per 32
-    // physical offset of logical float y (y % 4 == 0 chunks never straddle)
-    static __device__ __forceinline__ int phys(int y) { return y + ((y >> 5) << 2); }
+    static constexpr int L = MS + 2 * PADL;          // floats (multiple of 32)
+    static constexpr int PHYS = L;
+    static constexpr int SW = VL / 4 - 1;            // VL = 8: 1, VL = 16: 3
+    // physical offset of logical float y (4-float chunks stay contiguous)
+    static __device__ __forceinline__ int phys(int y) {
+        const int k = y >> 2;
+        return ((k ^ ((k >> 3) & SW)) << 2) | (y & 3);
+    }
 };
 
 __device__ __forceinline__ float4 lds128(const float *p) {
@@ -57,7 +66,7 @@ template <int DOM, int VL, int LP, int R, int O>
 __device__ __forceinline__ bool tap_message(const BandArgs &a, const float (&h)[VL], int x0,
                                             float *row, float (&out)[VL]) {
     static_assert(R % 4 == 0 && VL % 4 == 0, "4-tap chunks");
-    using Row = TapRow<VL * LP>;
+    using Row = TapRow<VL * LP, VL>;
     // publish h: the previous message's reads of the row are complete
     __syncwarp();
 #pragma unroll
@@ -251,7 +260,7 @@ constexpr int TAP_WARPS = 4;
 template <int VL, int LP, int NS>
 struct TapSmem {
     static constexpr int PPW = 32 / LP;
-    static constexpr int ROWF = TapRow<VL * LP>::PHYS;
+    static constexpr int ROWF = TapRow<VL * LP, VL>::PHYS;
     static constexpr int ROWS_F = PPW * ROWF;                  // floats of the rows
     static constexpr int STAGE_F = NS * 5 * 32 * VL;           // floats of the input stages
     static constexpr int WARP_F = (ROWS_F + 31) / 32 * 32 + STAGE_F;
@@ -262,7 +271,7 @@ struct TapSmem {
 // identity's absorbing value (0 for sums, -inf for maxima).  Written once.
 template <int DOM, int VL, int LP>
 __device__ __forceinline__ void tap_rows_init(float *rows) {
-    using Row = TapRow<VL * LP>;
+    using Row = TapRow<VL * LP, VL>;
     constexpr int PPW = 32 / LP;
     constexpr float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
     const int lane = threadIdx.x & 31;
@@ -290,7 +299,7 @@ band_iter_tap_kernel(const __grid_constant__ BandArgs a) {
     const int j = lane % LP, q = lane / LP;
     const int x0 = j * VL;
     float *wbase = tap_smem + warp * SM::WARP_F;
-    float *row = wbase + q * TapRow<VL * LP>::PHYS;
+    float *row = wbase + q * TapRow<VL * LP, VL>::PHYS;
     float *buf = wbase + (SM::ROWS_F + 31) / 32 * 32;
     tap_rows_init<DOM, VL, LP>(wbase);
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
@@ -409,6 +418,7 @@ cudaError_t launch_band_tap(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
+    if (launch_block_cap() > 0 && blocks > launch_block_cap()) blocks = launch_block_cap();
     band_iter_tap_kernel<DOM, VL, LP, R, ROLLED, NS><<<(unsigned)blocks, 32 * TAP_WARPS, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -434,7 +444,7 @@ __device__ __forceinline__ float node_reduce(const float (&h)[VL]) {
 
 template <int DOM, int VL, int LP>
 __device__ __forceinline__ void put_row(float *row, int x0, const float (&h)[VL]) {
-    using Row = TapRow<VL * LP>;
+    using Row = TapRow<VL * LP, VL>;
 #pragma unroll
     for (int i = 0; i < VL; i += 4)
         sts128(row + Row::phys(Row::PADL + x0 + i), h[i], h[i + 1], h[i + 2], h[i + 3]);
@@ -444,7 +454,7 @@ __device__ __forceinline__ void put_row(float *row, int x0, const float (&h)[VL]
 template <int DOM, int VL, int LP, int R, int O>
 __device__ __forceinline__ bool tap2_message(const BandArgs &a, float red, int x0, const float *row,
                                              float (&out)[VL]) {
-    using Row = TapRow<VL * LP>;
+    using Row = TapRow<VL * LP, VL>;
     const float base = DOM == SBP_SUM ? (a.floor_term ? a.fbar[O] * red : 0.0f)
                                       : (a.floor_term ? a.fbar[O] + red : -__builtin_huge_valf());
 #pragma unroll
@@ -543,7 +553,7 @@ __device__ __forceinline__ void tap2_form_h(const float (&g)[VL], const float (&
                                             const float (&m1)[VL], const float (&m2)[VL],
                                             const float (&m3)[VL], int x0, float *rows,
                                             float (&red)[4]) {
-    constexpr int ROWF = TapRow<VL * LP>::PHYS;
+    constexpr int ROWF = TapRow<VL * LP, VL>::PHYS;
     float h[VL];
     if (DOM == SBP_SUM) {
         // reference order: unary, slots 0..3 ascending skipping the excluded
@@ -593,17 +603,19 @@ __device__ __forceinline__ void tap2_form_h(const float (&g)[VL], const float (&
     }
 }
 
-template <int VL, int LP>
+template <int VL, int LP, int STG>
 struct Tap2Smem {
     static constexpr int PPW = 32 / LP;
-    static constexpr int ROWF = TapRow<VL * LP>::PHYS;
-    static constexpr int WARP_F = (PPW * 4 * ROWF + 31) / 32 * 32;
+    static constexpr int ROWF = TapRow<VL * LP, VL>::PHYS;
+    static constexpr int ROWS_F = (PPW * 4 * ROWF + 31) / 32 * 32;
+    static constexpr int STAGE_F = STG ? 5 * 32 * VL : 0;   // next group's 5 input vectors
+    static constexpr int WARP_F = ROWS_F + STAGE_F;
     static constexpr size_t bytes() { return (size_t)TAP_WARPS * WARP_F * sizeof(float); }
 };
 
 template <int DOM, int VL, int LP>
 __device__ __forceinline__ void tap2_rows_init(float *wbase) {
-    using Row = TapRow<VL * LP>;
+    using Row = TapRow<VL * LP, VL>;
     constexpr int NROWS = 4 * (32 / LP);
     constexpr float PAD = DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf();
     const int lane = threadIdx.x & 31;
@@ -619,26 +631,60 @@ __device__ __forceinline__ void tap2_rows_init(float *wbase) {
 #ifndef SBP_TAP2_BLOCKS
 #define SBP_TAP2_BLOCKS 8
 #endif
-template <int DOM, int VL, int LP, int R, bool ROLLED>
-__global__ void __launch_bounds__(32 * TAP_WARPS, (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6))
+// STG = 1: the next pixel group's five input vectors are fetched into shared
+// memory by the tensor-memory accelerator (1-D bulk copies on an mbarrier)
+// while the current group computes, instead of register loads whose latency
+// the first products of the group wait on (ncu: 10 % of the samples of the
+// register-loaded kernel stall on the first FMUL2 of a group).
+template <int DOM, int VL, int LP, int R, bool ROLLED, int STG>
+__global__ void __launch_bounds__(32 * TAP_WARPS, (STG ? 5 : (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6)))
 band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
-    using SM = Tap2Smem<VL, LP>;
+    using SM = Tap2Smem<VL, LP, STG>;
     constexpr int PPW = 32 / LP;
     constexpr int ROWF = SM::ROWF;
+    constexpr int VEC = 32 * VL;
     float dmax = 0.0f;
     const IterCtx it = iter_of(a, &dmax);
     extern __shared__ __align__(128) float tap_smem[];
+    __shared__ __align__(8) unsigned long long bars[TAP_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j = lane % LP, q = lane / LP;
     const int x0 = j * VL;
     float *wbase = tap_smem + warp * SM::WARP_F;
     float *rows = wbase + q * 4 * ROWF;
+    float *stage = wbase + SM::ROWS_F;
     tap2_rows_init<DOM, VL, LP>(wbase);
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
     const long long ngroups = (npix + PPW - 1) / PPW;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; grp < ngroups;
-         grp += nwarps) {
+    long long grp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nvec = it.first ? 1 : 5;
+    auto issue = [&](long long gg) {
+        if (lane == 0) {
+            const long long p0 = gg * PPW;
+            const long long n = npix - p0 < PPW ? npix - p0 : PPW;
+            const unsigned bytes = (unsigned)(n * a.Ms * 4);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&bars[warp], bytes * nvec);
+            bulk_g2s(stage, a.values + ((long long)(a.lr_begin - 1) * a.W + p0) * a.Ms, bytes,
+                     &bars[warp]);
+            if (!it.first)
+                for (int k = 0; k < 4; ++k)
+                    bulk_g2s(stage + (1 + k) * VEC,
+                             it.msgs_in + k * a.slot_stride + ((long long)a.lr_begin * a.W + p0) * a.Ms,
+                             bytes, &bars[warp]);
+        }
+    };
+    unsigned phase = 0;
+    if constexpr (STG) {
+        if (lane == 0) {
+            mbar_init(&bars[warp], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        if (grp < ngroups) issue(grp);
+    }
+    for (; grp < ngroups; grp += nwarps) {
         long long p = grp * PPW + q;
         const bool valid = p < npix;
         if (!valid) p = npix - 1;
@@ -649,14 +695,33 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
         float red[4];
         {
             float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
-            Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
-            if (!it.first) {
-                const float *mi = it.msgs_in + node_l * a.Ms + x0;
-                Vec8Loader<VL>::load(m0, mi);
-                Vec8Loader<VL>::load(m1, mi + a.slot_stride);
-                Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
-                Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+            if constexpr (STG) {
+                mbar_wait(&bars[warp], phase);
+                phase ^= 1u;
+                const float *src = stage + q * a.Ms + x0;
+                float *mm[5] = {g, m0, m1, m2, m3};
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    if (k > 0 && it.first) break;
+#pragma unroll
+                    for (int i = 0; i < VL; i += 4) {
+                        const float4 v = *reinterpret_cast<const float4 *>(src + k * VEC + i);
+                        mm[k][i] = v.x; mm[k][i + 1] = v.y; mm[k][i + 2] = v.z; mm[k][i + 3] = v.w;
+                    }
+                }
+                __syncwarp();   // every lane has its inputs: refill the stage
+                if (grp + nwarps < ngroups) issue(grp + nwarps);
             } else {
+                Vec8Loader<VL>::load(g, a.values + ((long long)(lr - 1) * a.W + c) * a.Ms + x0);
+                if (!it.first) {
+                    const float *mi = it.msgs_in + node_l * a.Ms + x0;
+                    Vec8Loader<VL>::load(m0, mi);
+                    Vec8Loader<VL>::load(m1, mi + a.slot_stride);
+                    Vec8Loader<VL>::load(m2, mi + 2 * a.slot_stride);
+                    Vec8Loader<VL>::load(m3, mi + 3 * a.slot_stride);
+                }
+            }
+            if (it.first) {
                 const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
                 float *mm[4] = {m0, m1, m2, m3};
 #pragma unroll
@@ -667,7 +732,7 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
                         mm[k][i] = x0 + i < a.M ? real : (DOM == SBP_SUM ? 0.0f : -__builtin_huge_valf());
                 }
             }
-            __syncwarp();   // the previous node's messages are done reading the rows
+            __syncwarp();   // the previous group's messages are done reading the rows
             tap2_form_h<DOM, VL, LP>(g, m0, m1, m2, m3, x0, rows, red);
         }
         __syncwarp();
@@ -700,19 +765,19 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
     if (a.delta) flush_delta(a.delta, dmax);
 }
 
-template <int DOM, int VL, int LP, int R, bool ROLLED>
+template <int DOM, int VL, int LP, int R, bool ROLLED, int STG>
 cudaError_t launch_band_tap2(const BandArgs &a, cudaStream_t s) {
     constexpr int PPW = 32 / LP;
-    const size_t smem = Tap2Smem<VL, LP>::bytes();
+    const size_t smem = Tap2Smem<VL, LP, STG>::bytes();
     static int resident = 0, sms = 0;
     if (!resident) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED>,
+        cudaFuncSetAttribute(band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED, STG>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &resident, band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED>, 32 * TAP_WARPS, smem);
+            &resident, band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED, STG>, 32 * TAP_WARPS, smem);
         if (resident < 1) resident = 1;
     }
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
@@ -721,7 +786,8 @@ cudaError_t launch_band_tap2(const BandArgs &a, cudaStream_t s) {
     if (blocks <= 0) return cudaSuccess;
     const long long cap = (long long)sms * resident;
     if (blocks > cap) blocks = cap;
-    band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED><<<(unsigned)blocks, 32 * TAP_WARPS, smem, s>>>(a);
+    if (launch_block_cap() > 0 && blocks > launch_block_cap()) blocks = launch_block_cap();
+    band_iter_tap2_kernel<DOM, VL, LP, R, ROLLED, STG><<<(unsigned)blocks, 32 * TAP_WARPS, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -735,8 +801,11 @@ BandLaunchFn pick_band_tap(int vl, int R, bool rolled, int staged) {
 #define SBP_TAP(RR)                                                                          \
     if (R == RR) {                                                                           \
         if (vl == 8 && staged == 2)                                                          \
-            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true>                      \
-                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false>;                    \
+            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true, 0>                   \
+                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false, 0>;                 \
+        if (vl == 8 && staged == 3)                                                          \
+            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true, 1>                   \
+                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false, 1>;                 \
         if (vl == 8) {                                                                       \
             if (rolled) return staged ? &launch_band_tap<DOM, 8, MS / 8, RR, true, 2>        \
                                       : &launch_band_tap<DOM, 8, MS / 8, RR, true, 0>;       \

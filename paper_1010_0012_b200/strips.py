@@ -136,7 +136,7 @@ class StripRunner:
 
 
 def run_rank(strip, iters: int, rank: int, world: int, group=None, overlap: bool = True,
-             compute_stream=None, interior_stream=None, dist=None) -> None:
+             compute_stream=None, interior_stream=None, dist=None, timing: list | None = None) -> None:
     """Per-rank loop of the distributed strip decomposition.
 
     ``strip`` is this rank's strip (rank k owns strip k, top to bottom).
@@ -144,15 +144,25 @@ def run_rank(strip, iters: int, rank: int, world: int, group=None, overlap: bool
     gloo.  When ``overlap`` is set and streams are given, the interior rows run
     on ``interior_stream`` while the halos travel.  ``dist`` defaults to
     ``torch.distributed`` (tests substitute an in-process transport).
+
+    ``timing`` (CUDA only): a list that receives one ``IterEvents`` per
+    iteration -- boundary rows, halo arrival, interior rows, end -- so the
+    caller can split the iteration into compute / exchange / overlap.
     """
     if dist is None:
         import torch.distributed as dist
 
     boundary, interior = _split_rows(strip.rows)
     cuda = strip.next_buffer().is_cuda
+    rec = timing is not None and cuda
     for _ in range(iters):
+        if rec:
+            ev = IterEvents()
+            ev.start.record()
         for lo, hi in boundary:
             strip.compute(lo, hi)
+        if rec:
+            ev.boundary.record()
         ops = []
         h = halo_views(strip.next_buffer(), strip.rows)
         if rank + 1 < world:
@@ -162,14 +172,57 @@ def run_rank(strip, iters: int, rank: int, world: int, group=None, overlap: bool
             ops.append(dist.P2POp(dist.isend, h["send_up"], rank - 1, group))
             ops.append(dist.P2POp(dist.irecv, h["recv_above"], rank - 1, group))
         reqs = dist.batch_isend_irecv(ops) if ops else []
+        joined = True
         if interior is not None:
             if cuda and overlap and interior_stream is not None:
                 interior_stream.wait_stream(torch.cuda.current_stream())
                 with torch.cuda.stream(interior_stream):
+                    if rec:
+                        ev.interior_start.record(interior_stream)
                     strip.compute(*interior, stream=interior_stream)
-                torch.cuda.current_stream().wait_stream(interior_stream)
+                    if rec:
+                        ev.interior_end.record(interior_stream)
+                joined = False
             else:
                 strip.compute(*interior)
         for r in reqs:
             r.wait()
+        if rec:
+            ev.halo.record()          # the halos have landed (stream-ordered wait)
+        if not joined:
+            torch.cuda.current_stream().wait_stream(interior_stream)
+        if rec:
+            ev.end.record()
+            timing.append(ev)
         strip.flip()
+
+
+class IterEvents:
+    """CUDA events of one strip iteration (see run_rank)."""
+
+    def __init__(self):
+        mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        self.start, self.boundary, self.halo, self.end = mk(), mk(), mk(), mk()
+        self.interior_start, self.interior_end = mk(), mk()
+
+    def split(self) -> dict:
+        """ms: boundary rows, exchange (boundary done -> halos landed),
+        interior rows, whole iteration, and the exchange time NOT hidden
+        behind the interior rows."""
+        b = self.start.elapsed_time(self.boundary)
+        x = self.boundary.elapsed_time(self.halo)
+        try:
+            i = self.interior_start.elapsed_time(self.interior_end)
+        except RuntimeError:          # no interior rows (strips of <= 2 rows)
+            i = 0.0
+        t = self.start.elapsed_time(self.end)
+        return {"boundary_ms": b, "exchange_ms": x, "interior_ms": i, "iteration_ms": t,
+                "exposed_exchange_ms": max(0.0, t - b - i)}
+
+
+def summarize_timing(timing: list) -> dict:
+    """Median per-iteration split over a run's IterEvents (after a sync)."""
+    rows = [e.split() for e in timing]
+    if not rows:
+        return {}
+    return {k: float(np.median([r[k] for r in rows])) for k in rows[0]}

@@ -15,7 +15,8 @@ torch = pytest.importorskip("torch")
 
 import paper_1010_0012_b200 as sbp  # noqa: E402
 from paper_1010_0012_b200 import synth  # noqa: E402
-from paper_1010_0012_b200.strips import GpuStrip, partition_rows, run_rank  # noqa: E402
+from paper_1010_0012_b200.strips import (GpuStrip, partition_rows, run_rank,  # noqa: E402
+                                         summarize_timing)
 
 pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
@@ -69,6 +70,7 @@ def test_threaded_ranks_match_whole_grid(world, domain):
     full = sbp.run_sweeps(model, iters, domain=domain, schedule="synchronous").engine.msgs4()
     fake = FakeDist()
     parts = [None] * world
+    splits = [None] * world
     errors = []
 
     def rank_main(rank):
@@ -77,9 +79,14 @@ def test_threaded_ranks_match_whole_grid(world, domain):
             r0, rows = partition_rows(H, world)[rank]
             strip = GpuStrip(model, r0, rows, domain, "fast")
             interior = torch.cuda.Stream()
+            timing = []
             with torch.cuda.stream(torch.cuda.Stream()):
-                run_rank(strip, iters, rank, world, interior_stream=interior, dist=fake)
+                run_rank(strip, iters, rank, world, interior_stream=interior, dist=fake,
+                         timing=timing)
                 torch.cuda.current_stream().synchronize()
+            interior.synchronize()
+            assert len(timing) == iters
+            splits[rank] = summarize_timing(timing)
             parts[rank] = strip.current_buffer()[:, 1:rows + 1, :, :model.M].double().cpu().numpy()
         except Exception as exc:   # surfaced below
             errors.append(exc)
@@ -92,6 +99,9 @@ def test_threaded_ranks_match_whole_grid(world, domain):
     assert not errors, errors
     got = np.concatenate(parts, axis=1).reshape(4, H * W, model.M)
     np.testing.assert_array_equal(got, full)
+    for sp in splits:     # per-rank compute / exchange / overlap split (bench --gpus N)
+        assert sp["iteration_ms"] > 0 and sp["boundary_ms"] > 0 and sp["interior_ms"] > 0
+        assert sp["exposed_exchange_ms"] <= sp["iteration_ms"]
 
 
 def test_run_sweeps_strips_single_rank():

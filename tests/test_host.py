@@ -293,3 +293,19 @@ def test_plan_name_reports_the_fallback(monkeypatch):
     assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=8,LP=16,R=7,rolled>"
     monkeypatch.setenv("SBP_ROLL_MIN_R", "99")
     assert _plan_name("C4", "sum") == "band_iter_kernel<sum,VL=8,LP=16,R=7>"
+
+
+@pytest.mark.parametrize("M,T", [(16, 10.0), (16, 12.0), (32, 18.0), (32, 30.0)])
+def test_band_without_compiled_radius_plans_as_ell(M, T):
+    """a Toeplitz band whose radius has no compiled kernel below Ms
+    (Ms=16, R=9..15; Ms=32, R=17..31) must plan the general ELL kernel, not a
+    band launch that fails with 'no band kernel'."""
+    pot = truncated_linear_potential(M, 0.5, T)
+    Ms = L.lib().sbp_padded_labels(M)
+    R, _ = plan.toeplitz_band(pot.col_indptr, pot.col_indices, pot.col_residuals, M, 0.0)
+    assert R > 8 and L.lib().sbp_band_radius(Ms, R) == 0
+    pl = plan.plan_potential(pot, "sum", "fast", M, Ms)
+    assert pl.kind == L.SBP_POT_ELL
+    # a compiled radius still plans as a band
+    assert plan.plan_potential(truncated_linear_potential(M, 0.5, 3.0), "sum", "fast", M,
+                               Ms).kind == L.SBP_POT_BAND

@@ -44,7 +44,7 @@ def model_for(name, extra):
     m = synth.build_config_model(synth.CONFIGS[name], height=H, width=W)
     if extra == "ell":
         d = m.shared_potential.densify().table.copy()
-        d[2, 4] *= 0.5
+        d[2, 4] = 0.5 * (d[2, 4] + 1.0)
         m = sbp.GridMrf(H, W, m.M, m.unaries, sbp.sparse_from_dense(d, fbar=m.shared_potential.fbar),
                         log_unaries=m.log_unaries)
     return m
