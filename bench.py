@@ -466,9 +466,16 @@ def configs_block(args, torch, dev):
         eng.step(2)
         torch.cuda.synchronize()
         evs: list = []
+        # runs of `iters` iterations from the initial messages, repeated for
+        # at least 0.5 s so the clock sampler sees the kernel under load
         with ClockSampler(dev.index) as clk:
-            eng.step(iters, events=evs)
-            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            while True:
+                eng.reset()
+                eng.step(iters, events=evs)
+                torch.cuda.synchronize()
+                if time.perf_counter() - t0 >= 0.5:
+                    break
         eng.raise_if_degenerate()
         per = sorted(a.elapsed_time(b) / k for a, b, k in evs)
         ms = per[len(per) // 2]

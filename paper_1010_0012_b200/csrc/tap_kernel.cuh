@@ -19,9 +19,9 @@
 //   (0 / -inf) on both sides, written once per launch, so no selects are
 //   needed, and taps never occupy more than one 4-float chunk of registers.
 //
-// Rows use an XOR-swizzled layout (TapRow) so the 8 lanes of each LDS.128 /
-// STS.128 phase hit 8 distinct 16-byte bank groups for both lane strides
-// used here (VL = 8 and 16): conflict-free.
+// Rows use a sub-row layout (TapRow) so the 8 lanes of each LDS.128 /
+// STS.128 phase read 8 consecutive 16-byte slots: conflict-free, and every
+// access is a per-lane base pointer plus an immediate offset.
 #pragma once
 
 #include "band_kernel.cuh"
@@ -29,20 +29,31 @@
 namespace sbp {
 
 // Row of one node's h in shared memory: PADL pad labels, Ms labels, PADL pad
-// labels.  16-byte chunks are XOR-swizzled within each 128-byte line group so
-// that the 8 lanes of an LDS.128 / STS.128 phase, which touch chunks
-// c, c + VL/4, ..., c + 7 VL/4 (lane stride VL labels), land in 8 distinct
-// bank groups for every c: chunk k lives at k ^ ((k >> 3) & (VL/4 - 1)).
+// labels, as 4-float chunks k.  Lane j owns chunks k = PADL/4 + S j + ...
+// (S = VL/4 chunks per lane), so the 8 lanes of an LDS.128 / STS.128 phase
+// touch chunks c, c + S, ..., c + 7 S.  The row is stored as S sub-rows by
+// k mod S (chunk k at (k / S) + (k mod S) * NCH/S): those 8 chunks are then 8
+// CONSECUTIVE 16-byte slots -- 8 distinct bank groups, conflict-free -- and,
+// because k mod S and the k / S offset depend only on the compile-time tap
+// offset, every access is the lane's base pointer plus an immediate.
 template <int MS, int VL>
 struct TapRow {
     static constexpr int PADL = 32;                  // >= SBP_MAX_R, multiple of 32
-    static constexpr int L = MS + 2 * PADL;          // floats (multiple of 32)
+    static constexpr int L = MS + 2 * PADL;          // floats
     static constexpr int PHYS = L;
-    static constexpr int SW = VL / 4 - 1;            // VL = 8: 1, VL = 16: 3
-    // physical offset of logical float y (4-float chunks stay contiguous)
+    static constexpr int S = VL / 4;                 // lane stride in chunks
+    static constexpr int NCH = L / 4;
+    static constexpr int QS = NCH / S;               // chunks per sub-row
+    static_assert(NCH % S == 0 && (PADL / 4) % S == 0, "sub-row layout");
+    // physical float offset of logical float y (row initialisation)
     static __device__ __forceinline__ int phys(int y) {
         const int k = y >> 2;
-        return ((k ^ ((k >> 3) & SW)) << 2) | (y & 3);
+        return 4 * ((k / S) + (k % S) * QS) + (y & 3);
+    }
+    // float offset, from the lane's base (row + 4 j), of the chunk holding the
+    // lane's labels x0 + t .. x0 + t + 3 (t a multiple of 4, |t| <= PADL)
+    static __device__ __forceinline__ constexpr int off(int t) {
+        return 4 * ((PADL / 4 + t / 4) / S + ((PADL / 4 + t / 4) % S) * QS);
     }
 };
 
@@ -71,7 +82,7 @@ __device__ __forceinline__ bool tap_message(const BandArgs &a, const float (&h)[
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < VL; i += 4)
-        sts128(row + Row::phys(Row::PADL + x0 + i), h[i], h[i + 1], h[i + 2], h[i + 3]);
+        sts128(row + 4 * (x0 / VL) + Row::off(i), h[i], h[i + 1], h[i + 2], h[i + 3]);
     if (DOM == SBP_SUM) {
         const float s = lanes_sum<LP>(vsum(h));
         const float base = a.floor_term ? a.fbar[O] * s : 0.0f;
@@ -95,7 +106,7 @@ __device__ __forceinline__ bool tap_message(const BandArgs &a, const float (&h)[
         if (tc >= 0 && tc < VL) {
             hv[0] = h[tc]; hv[1] = h[tc + 1]; hv[2] = h[tc + 2]; hv[3] = h[tc + 3];
         } else {
-            const float4 v = lds128(row + Row::phys(Row::PADL + x0 + tc));
+            const float4 v = lds128(row + 4 * (x0 / VL) + Row::off(tc));
             hv[0] = v.x; hv[1] = v.y; hv[2] = v.z; hv[3] = v.w;
         }
         if (DOM == SBP_SUM) {
@@ -447,7 +458,7 @@ __device__ __forceinline__ void put_row(float *row, int x0, const float (&h)[VL]
     using Row = TapRow<VL * LP, VL>;
 #pragma unroll
     for (int i = 0; i < VL; i += 4)
-        sts128(row + Row::phys(Row::PADL + x0 + i), h[i], h[i + 1], h[i + 2], h[i + 3]);
+        sts128(row + 4 * (x0 / VL) + Row::off(i), h[i], h[i + 1], h[i + 2], h[i + 3]);
 }
 
 // One message from the node's row of direction `dir` (floor reduction `red`).
@@ -461,7 +472,7 @@ __device__ __forceinline__ bool tap2_message(const BandArgs &a, float red, int x
     for (int i = 0; i < VL; ++i) out[i] = base;
 #pragma unroll
     for (int tc = -R; tc < VL + R; tc += 4) {
-        const float4 v = lds128(row + Row::phys(Row::PADL + x0 + tc));
+        const float4 v = lds128(row + 4 * (x0 / VL) + Row::off(tc));
         const float hv[4] = {v.x, v.y, v.z, v.w};
         if (DOM == SBP_SUM) {
 #pragma unroll

@@ -43,17 +43,25 @@ def main():
         r0, rows = partition_rows(cfg.height, n)[rank]
         values = synth.config_values(cfg, "sum", r0=r0, rows=rows)
         strip = GpuStrip(model, r0, rows, "sum", "fast", values=values)
+        # the null transport delivers no halos: give the halo rows (and every
+        # slot of both buffers) valid initial messages, else NaN garbage makes
+        # every message degenerate and the error-word atomics dominate
+        for b in strip.engine.msgs:
+            strip.engine._init(b, ghosts_only=False)
         interior = torch.cuda.Stream()
         d = NullDist()
         run_rank(strip, 5, rank, n, interior_stream=interior, dist=d)
         torch.cuda.synchronize()
         iters = 200
-        timing = []
         t0 = time.perf_counter()
+        run_rank(strip, iters, rank, n, interior_stream=interior, dist=d)
+        host = (time.perf_counter() - t0) / iters         # enqueue cost, no events
+        torch.cuda.synchronize()
+        timing = []
         run_rank(strip, iters, rank, n, interior_stream=interior, dist=d, timing=timing)
-        host = (time.perf_counter() - t0) / iters
         torch.cuda.synchronize()
         dev = summarize_timing(timing)
+        strip.engine.raise_if_degenerate()
         print(json.dumps({"n_gpus": n, "strip_rows": rows, "host_us_per_iteration": host * 1e6,
                           "device": dev, "kernel": strip.engine.kernel_name}), flush=True)
         del strip
