@@ -138,22 +138,30 @@ struct BandChoice {
     int rolled = 0, staged = 0;   // variant 3 only
 };
 
-// Shared-memory-tap kernel for wide bands: default off until the B200 A/B
-// picks it (SBP_TAP=1 forces it where compiled).
+// Shared-memory-tap kernels for wide bands (tap_kernel.cuh).  Defaults from
+// the B200 A/B (profiles/r02_ab_tap.md; ms per C5 iteration, shuffle kernel ->
+// tap kernel): R = 8 sum 1.625 -> 1.520 (v1, VL = 16), max 2.202 -> 2.052
+// (v2); R = 16 sum 2.046 -> 1.862, max 3.172 -> 2.778 (v2); R = 32 sum
+// 3.091 -> 2.831 (v2), max 4.816 -> 3.893 (v2 rolled: the unrolled four-copy
+// body overflows the instruction cache).  Knobs: SBP_TAP=0|1, SBP_TAP_VL,
+// SBP_TAP_STAGED (0..3, see below), SBP_TAP_ROLLED.
 bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     const EnvKnobs &k = knobs();
     const bool compiled = Ms >= 64 && (Rk == 8 || Rk == 16 || Rk == 32);
-    const int dflt = 0;
+    // default on where measured faster: every compiled wide band except the
+    // narrow R = 8 at Ms < 256 (C4-like grids keep the rolled VL = 16 band)
+    const int dflt = (Rk >= 16 || Ms >= 256) ? 1 : 0;
     if (!compiled || (k.tap < 0 ? dflt : k.tap) == 0) return false;
     c.variant = 3;
-    c.vl = (domain == SBP_SUM && Ms >= 128) ? 16 : 8;
-    if (k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128)) c.vl = k.tap_vl;
-    c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym) : (sym && Rk >= 32);
+    const bool v1_16 = domain == SBP_SUM && Ms >= 128 && Rk == 8;
+    c.vl = k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128) ? k.tap_vl
+                                                                               : (v1_16 ? 16 : 8);
+    c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym)
+                                 : (sym && Rk >= 32 && domain == SBP_MAX);
     // staged: 0 register-loaded inputs, 1 TMA-staged inputs, 2 register-light
     // v2 (all four exclusion vectors in shared-memory rows), 3 v2 with the next
     // group's inputs TMA-prefetched; 1..3 need VL = 8
-    c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0)
-                                 : (domain == SBP_MAX && c.vl == 8 ? 1 : 0);
+    c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0) : (c.vl == 8 ? 2 : 0);
     return true;
 }
 

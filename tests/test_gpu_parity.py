@@ -280,10 +280,10 @@ def _run_subprocess(env_extra, name, domain, iters, out):
 def test_rolled_and_unrolled_kernels_agree_bitwise(tmp_path, name, domain):
     """The rolled (one band copy) and unrolled kernels perform identical arithmetic."""
     # same lane width (VL=8) so both variants use the same reduction trees
-    a = _run_subprocess({"SBP_ROLL_MIN_R": "1", "SBP_BAND_VL": "8", "SBP_STAGED": "0"},
-                        name, domain, 7, tmp_path / "a.npy")
-    b = _run_subprocess({"SBP_ROLL_MIN_R": "99", "SBP_BAND_VL": "8", "SBP_STAGED": "0"},
-                        name, domain, 7, tmp_path / "b.npy")
+    a = _run_subprocess({"SBP_ROLL_MIN_R": "1", "SBP_BAND_VL": "8", "SBP_STAGED": "0",
+                         "SBP_TAP": "0"}, name, domain, 7, tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_ROLL_MIN_R": "99", "SBP_BAND_VL": "8", "SBP_STAGED": "0",
+                         "SBP_TAP": "0"}, name, domain, 7, tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
 
 
@@ -311,10 +311,10 @@ def test_device_stereo_unaries(domain):
 @pytest.mark.parametrize("name,domain", [("C4", "sum"), ("C3", "max"), ("C5_T9", "sum")])
 def test_staged_and_register_kernels_agree_bitwise(tmp_path, name, domain):
     """The TMA-staged variant only changes how inputs reach the registers."""
-    a = _run_subprocess({"SBP_STAGED": "1", "SBP_BAND_VL": "8"}, name, domain, 7,
-                        tmp_path / "a.npy")
-    b = _run_subprocess({"SBP_STAGED": "0", "SBP_BAND_VL": "8"}, name, domain, 7,
-                        tmp_path / "b.npy")
+    a = _run_subprocess({"SBP_STAGED": "1", "SBP_BAND_VL": "8", "SBP_TAP": "0"}, name, domain,
+                        7, tmp_path / "a.npy")
+    b = _run_subprocess({"SBP_STAGED": "0", "SBP_BAND_VL": "8", "SBP_TAP": "0"}, name, domain,
+                        7, tmp_path / "b.npy")
     np.testing.assert_array_equal(a, b)
 
 
@@ -425,6 +425,8 @@ def test_reference_shaped_model_object(schedule):
     ("C5_T33", "sum", {"SBP_TAP_ROLLED": "1"}), ("C5_T33", "max", {"SBP_TAP_ROLLED": "1"}),
     ("C5_T17", "max", {"SBP_TAP_STAGED": "1"}), ("C5_T17", "sum", {"SBP_TAP_STAGED": "0"}),
     ("C5_T9", "max", {"SBP_TAP_STAGED": "0", "SBP_TAP_ROLLED": "0"}),
+    ("C5_T33", "sum", {"SBP_TAP_STAGED": "2"}), ("C5_T33", "max", {"SBP_TAP_STAGED": "2"}),
+    ("C5_T17", "sum", {"SBP_TAP_STAGED": "3"}), ("C5_T9", "max", {"SBP_TAP_STAGED": "3"}),
 ])
 def test_tap_and_shuffle_kernels_agree_bitwise(tmp_path, name, domain, variant):
     """The shared-memory-tap kernels (tap_kernel.cuh) only change how a lane

@@ -274,8 +274,12 @@ def test_default_fusion_policy(monkeypatch):
     ("C3", "max", "band_iter_staged_kernel<max,VL=8,LP=8,R=3>"),
     ("C2", "sum", "band_iter_kernel<sum,VL=8,LP=4,R=2>"),
     ("C5_T5", "sum", "band_iter_staged_kernel<sum,VL=16,LP=16,R=4>"),
-    ("C5_T9", "sum", "band_iter_kernel<sum,VL=16,LP=16,R=8,rolled>"),
-    ("C5_T17", "sum", "band_iter_staged_kernel<sum,VL=8,LP=32,R=16>"),
+    ("C5_T9", "sum", "band_iter_tap_kernel<sum,VL=16,LP=16,R=8>"),
+    ("C5_T9", "max", "band_iter_tap2_kernel<max,VL=8,LP=32,R=8>"),
+    ("C5_T17", "sum", "band_iter_tap2_kernel<sum,VL=8,LP=32,R=16>"),
+    ("C5_T17", "max", "band_iter_tap2_kernel<max,VL=8,LP=32,R=16>"),
+    ("C5_T33", "sum", "band_iter_tap2_kernel<sum,VL=8,LP=32,R=32>"),
+    ("C5_T33", "max", "band_iter_tap2_kernel<max,VL=8,LP=32,R=32,rolled>"),
 ])
 def test_default_kernel_choice(name, domain, expect):
     # host-only: names the instantiation sbp_iterate would launch
@@ -285,6 +289,7 @@ def test_default_kernel_choice(name, domain, expect):
 def test_plan_name_reports_the_fallback(monkeypatch):
     # plain VL=16 is not compiled for R=16: the launch falls back to VL=8 and
     # the reported name must say so (it did not, once)
+    monkeypatch.setenv("SBP_TAP", "0")
     monkeypatch.setenv("SBP_STAGED", "0")
     monkeypatch.setenv("SBP_BAND_VL", "16")
     assert _plan_name("C5_T17", "sum") == "band_iter_kernel<sum,VL=8,LP=32,R=16>"
