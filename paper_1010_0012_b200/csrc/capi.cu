@@ -31,8 +31,8 @@ BandLaunchFn pick_chain(int R, int vl);
 SBP_EXTERN(8) SBP_EXTERN(16) SBP_EXTERN(32) SBP_EXTERN(64) SBP_EXTERN(128) SBP_EXTERN(256)
 #undef SBP_EXTERN
 #define SBP_EXTERN_TAP(MSV)                                                                  \
-    extern template BandLaunchFn pick_band_tap<MSV, SBP_SUM>(int, int, bool, int);          \
-    extern template BandLaunchFn pick_band_tap<MSV, SBP_MAX>(int, int, bool, int);
+    extern template BandLaunchFn pick_band_tap<MSV, SBP_SUM>(int, int, int, int);           \
+    extern template BandLaunchFn pick_band_tap<MSV, SBP_MAX>(int, int, int, int);
 SBP_EXTERN_TAP(64) SBP_EXTERN_TAP(128) SBP_EXTERN_TAP(256)
 #undef SBP_EXTERN_TAP
 }
@@ -156,11 +156,14 @@ bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     const bool v1_16 = domain == SBP_SUM && Ms >= 128 && Rk == 8;
     c.vl = k.tap_vl == 8 || (k.tap_vl == 16 && domain == SBP_SUM && Ms >= 128) ? k.tap_vl
                                                                                : (v1_16 ? 16 : 8);
-    c.rolled = k.tap_rolled >= 0 ? (k.tap_rolled && sym)
-                                 : (sym && Rk >= 32 && domain == SBP_MAX);
+    // rolled: 0 four band copies, 1 one copy in a direction loop (symmetric
+    // potentials), 2 two copies in a loop of two (v2 only, symmetric)
+    c.rolled = k.tap_rolled >= 0 ? (sym ? k.tap_rolled : 0)
+                                 : (sym && Rk >= 32 && domain == SBP_MAX ? 1 : 0);
     // staged: 0 register-loaded inputs, 1 TMA-staged inputs, 2 register-light
     // v2 (all four exclusion vectors in shared-memory rows), 3 v2 with the next
-    // group's inputs TMA-prefetched; 1..3 need VL = 8
+    // group's inputs TMA-prefetched into shared memory, 4 v2 with them
+    // prefetched into L2; 1..4 need VL = 8
     c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0) : (c.vl == 8 ? 2 : 0);
     return true;
 }
@@ -215,7 +218,7 @@ sbp::BandLaunchFn band_fn(int Ms, int dom, int vl, int R, int rolled);
 
 // The launch function actually used: the chosen variant if compiled, else
 // the always-compiled register-loaded VL=8 kernel (ch is updated to match).
-sbp::BandLaunchFn tap_fn(int Ms, int dom, int vl, int R, bool rolled, int staged) {
+sbp::BandLaunchFn tap_fn(int Ms, int dom, int vl, int R, int rolled, int staged) {
     switch (Ms) {
     case 64: return dom == SBP_SUM ? sbp::pick_band_tap<64, SBP_SUM>(vl, R, rolled, staged)
                                    : sbp::pick_band_tap<64, SBP_MAX>(vl, R, rolled, staged);
@@ -633,8 +636,10 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
             if (ch.variant == 3)
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s%s>",
                          ch.staged >= 2 ? "band_iter_tap2_kernel" : "band_iter_tap_kernel", dom,
-                         ch.vl, g->Ms / ch.vl, Rk, ch.rolled ? ",rolled" : "",
-                         (ch.staged == 1 || ch.staged == 3) ? ",staged" : "");
+                         ch.vl, g->Ms / ch.vl, Rk,
+                         ch.rolled == 1 ? ",rolled" : ch.rolled == 2 ? ",rolled2" : "",
+                         (ch.staged == 1 || ch.staged == 3) ? ",staged"
+                                                            : ch.staged == 4 ? ",l2pf" : "");
             else
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
                          ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom,

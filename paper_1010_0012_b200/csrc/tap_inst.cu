@@ -7,5 +7,5 @@
 #endif
 
 namespace sbp {
-template BandLaunchFn pick_band_tap<SBP_MS, SBP_DOM>(int, int, bool, int);
+template BandLaunchFn pick_band_tap<SBP_MS, SBP_DOM>(int, int, int, int);
 }

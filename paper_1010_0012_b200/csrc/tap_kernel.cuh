@@ -619,7 +619,7 @@ struct Tap2Smem {
     static constexpr int PPW = 32 / LP;
     static constexpr int ROWF = TapRow<VL * LP, VL>::PHYS;
     static constexpr int ROWS_F = (PPW * 4 * ROWF + 31) / 32 * 32;
-    static constexpr int STAGE_F = STG ? 5 * 32 * VL : 0;   // next group's 5 input vectors
+    static constexpr int STAGE_F = STG == 1 ? 5 * 32 * VL : 0;   // next group's 5 input vectors
     static constexpr int WARP_F = ROWS_F + STAGE_F;
     static constexpr size_t bytes() { return (size_t)TAP_WARPS * WARP_F * sizeof(float); }
 };
@@ -645,10 +645,13 @@ __device__ __forceinline__ void tap2_rows_init(float *wbase) {
 // STG = 1: the next pixel group's five input vectors are fetched into shared
 // memory by the tensor-memory accelerator (1-D bulk copies on an mbarrier)
 // while the current group computes, instead of register loads whose latency
-// the first products of the group wait on (ncu: 10 % of the samples of the
-// register-loaded kernel stall on the first FMUL2 of a group).
-template <int DOM, int VL, int LP, int R, bool ROLLED, int STG>
-__global__ void __launch_bounds__(32 * TAP_WARPS, (STG ? 5 : (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6)))
+// the first products of the group wait on (ncu: 10-20 % of the samples of the
+// register-loaded kernel stall on the first FMUL2 of a group).  STG = 2: the
+// register loads stay, and the next group's vectors are prefetched into L2
+// (cp.async.bulk.prefetch) one group ahead -- no shared memory, no occupancy
+// cost.
+template <int DOM, int VL, int LP, int R, int ROLLED, int STG>
+__global__ void __launch_bounds__(32 * TAP_WARPS, (STG == 1 ? 5 : (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6)))
 band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
     using SM = Tap2Smem<VL, LP, STG>;
     constexpr int PPW = 32 / LP;
@@ -686,8 +689,24 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
                              bytes, &bars[warp]);
         }
     };
+    auto prefetch_l2 = [&](long long gg) {
+        if (lane == 0) {
+            const long long p0 = gg * PPW;
+            const long long n = npix - p0 < PPW ? npix - p0 : PPW;
+            const unsigned bytes = (unsigned)(n * a.Ms * 4);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             a.values + ((long long)(a.lr_begin - 1) * a.W + p0) * a.Ms),
+                         "r"(bytes) : "memory");
+            if (!it.first)
+                for (int k = 0; k < 4; ++k)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     it.msgs_in + k * a.slot_stride +
+                                     ((long long)a.lr_begin * a.W + p0) * a.Ms),
+                                 "r"(bytes) : "memory");
+        }
+    };
     unsigned phase = 0;
-    if constexpr (STG) {
+    if constexpr (STG == 1) {
         if (lane == 0) {
             mbar_init(&bars[warp], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -706,7 +725,10 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
         float red[4];
         {
             float g[VL], m0[VL], m1[VL], m2[VL], m3[VL];
-            if constexpr (STG) {
+            if constexpr (STG == 2) {
+                if (grp + nwarps < ngroups) prefetch_l2(grp + nwarps);
+            }
+            if constexpr (STG == 1) {
                 mbar_wait(&bars[warp], phase);
                 phase ^= 1u;
                 const float *src = stage + q * a.Ms + x0;
@@ -752,19 +774,28 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
         auto one = [&](int dir, float rd) {
             const bool hd = (has >> dir) & 1u;
             if (!__any_sync(SBP_FULL_MASK, valid && hd)) return;
-            if (ROLLED || dir == 0 || dir == 2)
+            if (ROLLED != 0 || dir == 0 || dir == 2)
                 tap2_emit<DOM, VL, LP, R, 0>(a, it, rd, rows + dir * ROWF, dir, j, x0, valid && hd,
                                              node_l, r, c);
             else
                 tap2_emit<DOM, VL, LP, R, 1>(a, it, rd, rows + dir * ROWF, dir, j, x0, valid && hd,
                                              node_l, r, c);
         };
-        if constexpr (ROLLED) {
+        if constexpr (ROLLED == 1) {
 #pragma unroll 1
             for (int k = 0; k < 4; ++k) {
                 const int dir = (0x2013 >> (4 * k)) & 0xF;   // order 3, 1, 0, 2
                 const float rd = dir == 0 ? red[0] : dir == 1 ? red[1] : dir == 2 ? red[2] : red[3];
                 one(dir, rd);
+            }
+        } else if constexpr (ROLLED == 2) {
+            // two band copies, a loop of two: half the instruction footprint
+            // of the unrolled body (which misses in the instruction cache for
+            // wide max-sum bands), half the loop overhead of the rolled one
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) {
+                one(k ? 0 : 3, k ? red[0] : red[3]);
+                one(k ? 2 : 1, k ? red[2] : red[1]);
             }
         } else {
             one(3, red[3]);
@@ -776,7 +807,7 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
     if (a.delta) flush_delta(a.delta, dmax);
 }
 
-template <int DOM, int VL, int LP, int R, bool ROLLED, int STG>
+template <int DOM, int VL, int LP, int R, int ROLLED, int STG>
 cudaError_t launch_band_tap2(const BandArgs &a, cudaStream_t s) {
     constexpr int PPW = 32 / LP;
     const size_t smem = Tap2Smem<VL, LP, STG>::bytes();
@@ -805,18 +836,24 @@ cudaError_t launch_band_tap2(const BandArgs &a, cudaStream_t s) {
 // Radii with a shared-memory-tap kernel (multiples of 4: 4-tap chunks).
 // variant: 0 register-loaded, 1 TMA-staged (2 stages), rolled or unrolled.
 template <int MS, int DOM>
-BandLaunchFn pick_band_tap(int vl, int R, bool rolled, int staged) {
+BandLaunchFn pick_band_tap(int vl, int R, int rolled, int staged) {
     if constexpr (MS < 64) {
         return nullptr;
     } else {
 #define SBP_TAP(RR)                                                                          \
     if (R == RR) {                                                                           \
-        if (vl == 8 && staged == 2)                                                          \
-            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true, 0>                   \
-                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false, 0>;                 \
-        if (vl == 8 && staged == 3)                                                          \
-            return rolled ? &launch_band_tap2<DOM, 8, MS / 8, RR, true, 1>                   \
-                          : &launch_band_tap2<DOM, 8, MS / 8, RR, false, 1>;                 \
+        if (vl == 8 && staged >= 2 && staged <= 4) {                                       \
+            const int stg = staged == 2 ? 0 : staged == 3 ? 1 : 2;                            \
+            const int rl = rolled == 1 ? 1 : rolled == 2 ? 2 : 0;                              \
+            if (stg == 0) return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 0>         \
+                               : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 0>         \
+                                         : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 0>;        \
+            if (stg == 1) return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 1>         \
+                                         : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 1>;        \
+            return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 2>                       \
+                 : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 2>                       \
+                           : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 2>;                      \
+        }                                                                                    \
         if (vl == 8) {                                                                       \
             if (rolled) return staged ? &launch_band_tap<DOM, 8, MS / 8, RR, true, 2>        \
                                       : &launch_band_tap<DOM, 8, MS / 8, RR, true, 0>;       \
