@@ -36,15 +36,17 @@ FALLBACK_HBM_GBS = 6650.0                               # B200_PROFILING.md fall
 
 
 def fp32_peak():
-    """FP32 ceiling (TFLOP/s): the measured FFMA rate and, for max-sum, the
-    measured FADD2 + FMNMX3 rate (one add and one max per band candidate,
-    tools/pipes.cu), from the committed microbenchmark record; else nominal."""
+    """FP32 ceilings (T op/s) from the committed microbenchmark record
+    (profiles/fp32_peaks.json): the measured FFMA rate -- the roofline
+    denominator of both domains -- and, for max-sum, the measured rate of the
+    band's own FADD2 + FMNMX3 instruction stream (one add and one max per
+    band candidate), reported beside it; else the nominal FFMA peak."""
     p = ROOT / "profiles" / "fp32_peaks.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"sum": float(d["ffma_tflops"]), "max": float(d["add_max_tops"]),
+        return {"ffma": float(d["ffma_tflops"]), "add_max": float(d["add_max_tops"]),
                 "source": f"measured ({p.name}: {d.get('how', '')})"}
-    return {"sum": FP32_NOMINAL_TFLOPS, "max": FP32_NOMINAL_TFLOPS,
+    return {"ffma": FP32_NOMINAL_TFLOPS, "add_max": FP32_NOMINAL_TFLOPS,
             "source": "nominal 148 SM x 128 lanes x 2 x 1.965 GHz"}
 
 
@@ -431,6 +433,7 @@ def run_ours(args, cfg):
                      "l2_gbs": (B * levels / world) / (launch_ms / 1e3) / 1e9,
                      "flops_per_launch": F * levels / world,
                      "fp32_frac_nominal": (F / world) / (kern_ms / 1e3) / 1e12 / FP32_NOMINAL_TFLOPS,
+                     "fp32_frac_measured": (F / world) / (kern_ms / 1e3) / 1e12 / fp32_peak()["ffma"],
                      "sustained_copy_gbs": sus,
                      "frac_of_sustained_copy": achieved / sus if sus else None},
         "cpu_baseline": cpu,
@@ -458,7 +461,8 @@ def configs_block(args, torch, dev):
     from paper_1010_0012_b200.engine import GridEngine
     hbm, _ = peaks()
     fp = fp32_peak()
-    out = {"hbm_peak_gbs": hbm, "fp32_peak_tflops": {"sum": fp["sum"], "max": fp["max"]},
+    out = {"hbm_peak_gbs": hbm, "fp32_peak_tflops": fp["ffma"],
+           "max_sum_band_ceiling_tops": fp["add_max"],
            "fp32_peak_source": fp["source"], "entries": []}
 
     def measure(eng, iters, cfg, domain, kernel):
@@ -484,16 +488,20 @@ def configs_block(args, torch, dev):
         if kernel == "standard":
             F = cfg.n_directed * 2 * cfg.M * cfg.M
         t_hbm = B / (hbm * 1e9) * 1e3
-        t_fp = F / (fp[domain] * 1e12) * 1e3
+        t_fp = F / (fp["ffma"] * 1e12) * 1e3
         bound = "hbm" if t_hbm >= t_fp else "fp32"
+        roof = {"bound": bound, "ms": max(t_hbm, t_fp), "frac": max(t_hbm, t_fp) / ms,
+                "hbm_frac": t_hbm / ms, "fp32_frac": t_fp / ms}
+        if domain == "max" and kernel == "fast":
+            # the max-sum band issues one FADD2 half + one FMNMX3 half per
+            # candidate; its own instruction stream peaks below FFMA
+            t_im = F / (fp["add_max"] * 1e12) * 1e3
+            roof["band_ceiling_frac"] = max(t_hbm, t_im) / ms
         return {"config": cfg.name, "domain": domain, "kernel": kernel,
                 "kernel_name": eng.kernel_name, "iterations": iters,
                 "ms_per_iteration": ms, "updates_per_s": cfg.n_directed / ms * 1e3,
                 "bytes_per_iteration": B, "flops_per_iteration": F,
-                "roofline": {"bound": bound, "ms": max(t_hbm, t_fp),
-                             "frac": max(t_hbm, t_fp) / ms, "hbm_frac": t_hbm / ms,
-                             "fp32_frac": t_fp / ms},
-                "clocks": clk.summary()}
+                "roofline": roof, "clocks": clk.summary()}
 
     cfg = synth.CONFIGS["C3"]
     eng = GridEngine(synth.StripModel(cfg), "max", "fast", device=dev,

@@ -163,7 +163,8 @@ bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     // staged: 0 register-loaded inputs, 1 TMA-staged inputs, 2 register-light
     // v2 (all four exclusion vectors in shared-memory rows), 3 v2 with the next
     // group's inputs TMA-prefetched into shared memory, 4 v2 with them
-    // prefetched into L2; 1..4 need VL = 8
+    // prefetched into L2, 5 v2 with them double-buffered in registers; 1..5
+    // need VL = 8
     c.staged = k.tap_staged >= 0 ? (c.vl == 8 ? k.tap_staged : 0) : (c.vl == 8 ? 2 : 0);
     return true;
 }
@@ -639,7 +640,7 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
                          ch.vl, g->Ms / ch.vl, Rk,
                          ch.rolled == 1 ? ",rolled" : ch.rolled == 2 ? ",rolled2" : "",
                          (ch.staged == 1 || ch.staged == 3) ? ",staged"
-                                                            : ch.staged == 4 ? ",l2pf" : "");
+                         : ch.staged == 4 ? ",l2pf" : ch.staged == 5 ? ",regpf" : "");
             else
                 snprintf(buf, len, "%s<%s,VL=%d,LP=%d,R=%d%s>",
                          ch.variant == 2 ? "band_iter_staged_kernel" : "band_iter_kernel", dom,

@@ -649,9 +649,12 @@ __device__ __forceinline__ void tap2_rows_init(float *wbase) {
 // register-loaded kernel stall on the first FMUL2 of a group).  STG = 2: the
 // register loads stay, and the next group's vectors are prefetched into L2
 // (cp.async.bulk.prefetch) one group ahead -- no shared memory, no occupancy
-// cost.
+// cost.  STG = 3: register double buffering -- the next group's loads are
+// issued right after this group's exclusion vectors are formed and land
+// while its four messages are computed (+40 registers: 5 / 4 blocks per SM).
 template <int DOM, int VL, int LP, int R, int ROLLED, int STG>
-__global__ void __launch_bounds__(32 * TAP_WARPS, (STG == 1 ? 5 : (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6)))
+__global__ void __launch_bounds__(32 * TAP_WARPS, (STG == 1 ? 5 : STG == 3 ? (DOM == SBP_SUM ? 5 : 4)
+                                                   : (DOM == SBP_SUM ? SBP_TAP2_BLOCKS : 6)))
 band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
     using SM = Tap2Smem<VL, LP, STG>;
     constexpr int PPW = 32 / LP;
@@ -705,6 +708,22 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
                                  "r"(bytes) : "memory");
         }
     };
+    float ng[VL], nm[4][VL];   // STG == 3: the next group's inputs, in flight
+    auto load_regs = [&](long long gg) {
+        long long pp = gg * PPW + q;
+        if (pp >= npix) pp = npix - 1;
+        const int lr2 = it.lr_begin + (int)(pp / a.W);
+        const int c2 = (int)(pp % a.W);
+        Vec8Loader<VL>::load(ng, a.values + ((long long)(lr2 - 1) * a.W + c2) * a.Ms + x0);
+        if (!it.first) {
+            const float *mi = it.msgs_in + ((long long)lr2 * a.W + c2) * a.Ms + x0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) Vec8Loader<VL>::load(nm[k], mi + k * a.slot_stride);
+        }
+    };
+    if constexpr (STG == 3) {
+        if (grp < ngroups) load_regs(grp);
+    }
     unsigned phase = 0;
     if constexpr (STG == 1) {
         if (lane == 0) {
@@ -728,7 +747,13 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
             if constexpr (STG == 2) {
                 if (grp + nwarps < ngroups) prefetch_l2(grp + nwarps);
             }
-            if constexpr (STG == 1) {
+            if constexpr (STG == 3) {
+#pragma unroll
+                for (int i = 0; i < VL; ++i) {
+                    g[i] = ng[i];
+                    m0[i] = nm[0][i]; m1[i] = nm[1][i]; m2[i] = nm[2][i]; m3[i] = nm[3][i];
+                }
+            } else if constexpr (STG == 1) {
                 mbar_wait(&bars[warp], phase);
                 phase ^= 1u;
                 const float *src = stage + q * a.Ms + x0;
@@ -767,6 +792,9 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
             }
             __syncwarp();   // the previous group's messages are done reading the rows
             tap2_form_h<DOM, VL, LP>(g, m0, m1, m2, m3, x0, rows, red);
+            if constexpr (STG == 3) {
+                if (grp + nwarps < ngroups) load_regs(grp + nwarps);
+            }
         }
         __syncwarp();
         const unsigned has = (c + 1 < a.W ? 1u : 0u) | (c > 0 ? 2u : 0u) |
@@ -842,17 +870,20 @@ BandLaunchFn pick_band_tap(int vl, int R, int rolled, int staged) {
     } else {
 #define SBP_TAP(RR)                                                                          \
     if (R == RR) {                                                                           \
-        if (vl == 8 && staged >= 2 && staged <= 4) {                                       \
-            const int stg = staged == 2 ? 0 : staged == 3 ? 1 : 2;                            \
+        if (vl == 8 && staged >= 2 && staged <= 5) {                                       \
+            const int stg = staged == 2 ? 0 : staged == 3 ? 1 : staged == 4 ? 2 : 3;         \
             const int rl = rolled == 1 ? 1 : rolled == 2 ? 2 : 0;                              \
             if (stg == 0) return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 0>         \
                                : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 0>         \
                                          : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 0>;        \
             if (stg == 1) return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 1>         \
                                          : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 1>;        \
-            return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 2>                       \
-                 : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 2>                       \
-                           : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 2>;                      \
+            if (stg == 2) return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 2>         \
+                               : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 2>         \
+                                         : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 2>;        \
+            return rl == 1 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 1, 3>                       \
+                 : rl == 2 ? &launch_band_tap2<DOM, 8, MS / 8, RR, 2, 3>                       \
+                           : &launch_band_tap2<DOM, 8, MS / 8, RR, 0, 3>;                      \
         }                                                                                    \
         if (vl == 8) {                                                                       \
             if (rolled) return staged ? &launch_band_tap<DOM, 8, MS / 8, RR, true, 2>        \
