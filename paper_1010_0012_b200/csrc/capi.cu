@@ -114,6 +114,7 @@ struct EnvKnobs {
     int tap_staged = env_int_raw("SBP_TAP_STAGED", -1);
     int tap_rolled = env_int_raw("SBP_TAP_ROLLED", -1);
     int max_blocks = env_int_raw("SBP_MAX_BLOCKS", 0);
+    int tap_lift = env_int_raw("SBP_TAP_LIFT", 1);   // sum, Ms >= 128: R = 5..7 bands run on the R = 8 tap kernel
 };
 EnvKnobs &knobs() {
     static EnvKnobs k;
@@ -130,6 +131,13 @@ int env_int(const char *name, int dflt) {
     else return env_int_raw(name, dflt);
     return v < 0 ? dflt : v;
 }
+
+// Compiled radius a band of radius R runs on in the synchronous kernels (0:
+// none).  Sum-product bands of radius 5..7 at Ms >= 128 (C4: R = 7) are padded
+// to 8 with zero taps -- exact no-ops -- so the shared-memory-tap kernel
+// (R in {8, 16, 32}) applies: C4 2.27 vs 2.38 ms cold, 2.37 vs 2.46 sustained
+// (profiles/r02_ab_c4_tap.txt).  SBP_TAP_LIFT=0 or SBP_TAP=0 keeps R = 7.
+int kernel_radius(int Ms, int R, int domain);
 
 struct BandChoice {
     int vl;       // labels per lane
@@ -148,9 +156,10 @@ struct BandChoice {
 bool tap_choice(int Ms, int domain, int Rk, bool sym, BandChoice &c) {
     const EnvKnobs &k = knobs();
     const bool compiled = Ms >= 64 && (Rk == 8 || Rk == 16 || Rk == 32);
-    // default on where measured faster: every compiled wide band except the
-    // narrow R = 8 at Ms < 256 (C4-like grids keep the rolled VL = 16 band)
-    const int dflt = (Rk >= 16 || Ms >= 256) ? 1 : 0;
+    // default on where measured faster: every compiled wide band, and R = 8
+    // for sum-product at Ms >= 128 (v1, VL = 16: C4 and C5 T=9); max-sum R = 8
+    // at Ms < 256 keeps the staged shuffle kernel (not measured)
+    const int dflt = (Rk >= 16 || Ms >= 256 || (domain == SBP_SUM && Ms >= 128)) ? 1 : 0;
     if (!compiled || (k.tap < 0 ? dflt : k.tap) == 0) return false;
     c.variant = 3;
     const bool v1_16 = domain == SBP_SUM && Ms >= 128 && Rk == 8;
@@ -277,6 +286,14 @@ void band_args(const sbp_grid *g, const sbp_potential *pot, int Rk, const float 
         for (int d = -pot->R; d <= pot->R; ++d) a->w[o][d + Rk] = pot->band_w[o][d + pot->R];
     }
     sbp::band_pairs(*a, Rk, pad);
+}
+
+int kernel_radius(int Ms, int R, int domain) {
+    if (knobs().tap_lift && knobs().tap != 0 && domain == SBP_SUM && R >= 5 && R < 8 && Ms >= 128)
+        return 8;
+    for (int r : kRadii)
+        if (r >= R && r < Ms) return r;
+    return 0;
 }
 
 int band_radius(const sbp_grid *g, const sbp_potential *pot) {
@@ -444,9 +461,7 @@ static int iterate_impl(const sbp_grid *g, const sbp_potential *pot, const float
         if (pot->accumulate != SBP_ACC_F32)
             return fail(SBP_EUNSUPPORTED, "band kernels accumulate in f32 (plan ELL for f64)");
         if (pot->R < 0 || pot->R > SBP_MAX_R) return fail(SBP_EINVAL, "band radius %d", pot->R);
-        int Rk = 0;
-        for (int r : kRadii)
-            if (r >= pot->R && r < g->Ms) { Rk = r; break; }
+        const int Rk = kernel_radius(g->Ms, pot->R, pot->domain);
         BandChoice ch = band_choice(g->Ms, pot->domain, Rk, band_symmetric(pot));
         sbp::BandLaunchFn fn = Rk ? band_resolve(g->Ms, pot->domain, Rk, ch) : nullptr;
         if (!fn)
@@ -620,9 +635,8 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
     if (!pot || !buf || len < 1) return fail(SBP_EINVAL, "NULL pointer");
     const char *dom = pot->domain == SBP_SUM ? "sum" : "max";
     if (pot->kind == SBP_POT_BAND) {
-        int Rk = 0;
-        for (int r : kRadii)
-            if (r >= pot->R && r < g->Ms) { Rk = r; break; }
+        // the chain and fused kernels run on the plain compiled radius
+        const int Rk = sequential ? band_radius(g, pot) : kernel_radius(g->Ms, pot->R, pot->domain);
         if (sequential == 1) {
             const int cvl = (env_int("SBP_CHAIN_VL", 8) == 16 && pot->domain == SBP_SUM &&
                              g->Ms >= 128 && Rk <= 8) ? 16 : 8;

@@ -40,7 +40,8 @@ FAMILIES = [
     # id, config, domain, schedule, env, kernel, potential kind
     ("band_reg", "C1", "sum", SYNCHRONOUS, {}, "fast", None),
     ("band_staged", "C3", "max", SYNCHRONOUS, {}, "fast", None),
-    ("band_rolled", "C4", "sum", SYNCHRONOUS, {}, "fast", None),
+    ("band_rolled", "C4", "sum", SYNCHRONOUS, {"SBP_TAP": "0"}, "fast", None),
+    ("tap_c4", "C4", "sum", SYNCHRONOUS, {}, "fast", None),     # R = 7 padded to the R = 8 tap kernel
     ("tap_reg", "C5_T9", "sum", SYNCHRONOUS, {"SBP_TAP": "1", "SBP_TAP_STAGED": "0"}, "fast", None),
     ("tap_staged", "C5_T17", "max", SYNCHRONOUS, {"SBP_TAP": "1", "SBP_TAP_VL": "8",
                                                    "SBP_TAP_STAGED": "1"}, "fast", None),

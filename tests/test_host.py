@@ -270,7 +270,7 @@ def test_default_fusion_policy(monkeypatch):
 
 
 @pytest.mark.parametrize("name,domain,expect", [
-    ("C4", "sum", "band_iter_kernel<sum,VL=16,LP=8,R=7,rolled>"),
+    ("C4", "sum", "band_iter_tap_kernel<sum,VL=16,LP=8,R=8>"),
     ("C3", "max", "band_iter_staged_kernel<max,VL=8,LP=8,R=3>"),
     ("C2", "sum", "band_iter_kernel<sum,VL=8,LP=4,R=2>"),
     ("C5_T5", "sum", "band_iter_staged_kernel<sum,VL=16,LP=16,R=4>"),
