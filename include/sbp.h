@@ -97,7 +97,10 @@ typedef struct {
     const float *dense_t[2];              /* DENSE: device [Ms][Ms] per orientation,
                                              f(x_i = k, x_j = x) at [k][x] (tiled kernel,
                                              Ms >= 32); smaller Ms runs the ELL arrays with
-                                             m_max = M, idx[k][x] = k */
+                                             m_max = M, idx[k][x] = k.  A symmetric table may
+                                             pass the SAME pointer twice: sum-product at
+                                             Ms = 128 / 256 then runs as a 3xTF32 GEMM on the
+                                             tensor cores (tcgen05; SBP_DENSE_TC=0: SIMT) */
     /* ELL per-edge (inhomogeneous) potentials, n_pot > 0: ell_idx[0] / ell_w[0]
      * point at [n_pot][2][m_max][Ms], fbar_all at [n_pot][2]; pid_h[r*W + c]
      * is the potential of edge (n, n+1), pid_v[r*W + c] of edge (n, n+W)

@@ -50,6 +50,10 @@ struct DenseArgs {
     const float *t[2];   // [Ms][Ms] per orientation: f(x_i = k, x_j = x) at [k][x]
 };
 cudaError_t launch_dense(int domain, const DenseArgs &a, cudaStream_t s);
+// Sum-product, symmetric table (t[0] serves both orientations), Ms = 128 or
+// 256: the same update as a 3xTF32 GEMM on the tensor cores (dense_tc_kernel.cu).
+bool dense_tc_supported(int Ms);
+cudaError_t launch_dense_tc(const DenseArgs &a, cudaStream_t s);
 
 
 

@@ -114,6 +114,7 @@ struct EnvKnobs {
     int tap_staged = env_int_raw("SBP_TAP_STAGED", -1);
     int tap_rolled = env_int_raw("SBP_TAP_ROLLED", -1);
     int max_blocks = env_int_raw("SBP_MAX_BLOCKS", 0);
+    int dense_tc = env_int_raw("SBP_DENSE_TC", 1);   // dense sum-product on the tensor cores (0: SIMT)
     int tap_lift = env_int_raw("SBP_TAP_LIFT", 1);   // sum, Ms >= 128: R = 5..7 bands run on the R = 8 tap kernel
 };
 EnvKnobs &knobs() {
@@ -294,6 +295,14 @@ int kernel_radius(int Ms, int R, int domain) {
     for (int r : kRadii)
         if (r >= R && r < Ms) return r;
     return 0;
+}
+
+// The dense sum-product update runs as a 3xTF32 GEMM on the tensor cores
+// (dense_tc_kernel.cu) when the table is symmetric -- the caller passes the
+// SAME device pointer for both orientations -- and Ms is 128 or 256.
+bool dense_on_tensor_cores(const sbp_grid *g, const sbp_potential *pot) {
+    return knobs().dense_tc != 0 && pot->domain == SBP_SUM && pot->n_pot == 0 &&
+           pot->dense_t[0] && pot->dense_t[0] == pot->dense_t[1] && sbp::dense_tc_supported(g->Ms);
 }
 
 int band_radius(const sbp_grid *g, const sbp_potential *pot) {
@@ -492,6 +501,8 @@ static int iterate_impl(const sbp_grid *g, const sbp_potential *pot, const float
         a.first = (flags & SBP_ITER_FIRST) ? 1 : 0;
         a.t[0] = pot->dense_t[0];
         a.t[1] = pot->dense_t[1];
+        if (dense_on_tensor_cores(g, pot))
+            return cuda_status(sbp::launch_dense_tc(a, s), "sbp_iterate(dense, tensor cores)");
         return cuda_status(sbp::launch_dense(pot->domain, a, s), "sbp_iterate(dense)");
     }
     if (pot->kind == SBP_POT_ELL || pot->kind == SBP_POT_DENSE) {
@@ -661,7 +672,10 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
                          ch.vl, g->Ms / ch.vl, Rk, ch.variant == 1 ? ",rolled" : "");
         }
     } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
-        snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
+        if (sequential == 0 && dense_on_tensor_cores(g, pot))
+            snprintf(buf, len, "dense_tc_kernel<sum,Ms=%d,3xTF32>", g->Ms);
+        else
+            snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
     } else {
         snprintf(buf, len, "%s<%s%s>", sequential == 1 ? "ell_chain_kernel" : "ell_iter_kernel", dom,
                  pot->accumulate == SBP_ACC_F64 ? ",f64" : "");

@@ -288,8 +288,11 @@ class GridEngine:
                 t = torch.from_numpy(np.ascontiguousarray(plan.dense_t, dtype=np.float32)).to(
                     self.device)
                 plan.device_arrays.append(t)
+                # a symmetric table passes ONE pointer for both orientations:
+                # libsbp then runs sum-product on the tensor cores (sbp.h)
+                sym = np.array_equal(plan.dense_t[0], plan.dense_t[1])
                 for o in range(2):
-                    s.dense_t[o] = t[o].data_ptr()
+                    s.dense_t[o] = t[0 if sym else o].data_ptr()
         return s
 
     def upload_stereo(self) -> None:
