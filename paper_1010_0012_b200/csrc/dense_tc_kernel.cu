@@ -12,58 +12,82 @@
 // orientations), Ms = 128 (one CTA) or Ms = 256 (a CTA pair, cta_group::2,
 // each CTA owning 128 of the 256 output labels).
 //
-// Layout per CTA:
-//   shared memory  f_hi rows of this CTA [128 x Ms] tf32, K-major, 128-byte swizzle (64 / 128 KB)
-//                  3 stages of the h tile: [32 / CG columns x Ms] hi and lo planes (32 KB each)
-//   tensor memory  columns [0, 96): 3 accumulator stages [128 labels x 32 columns] fp32
-//                  columns [128, 128 + Ms): f_lo rows of this CTA (the A operand of f_lo h_hi)
-// Warp roles (17 warps, one CTA per SM, persistent over tiles of 8 nodes):
+// Tile shape.  On B200 one tcgen05.mma kind::tf32 (K = 8) takes >= 67 cycles
+// whatever N <= 128 is (tools/tc_probe.cu mode 9, profiles/r02_tcgen05_mma_rate.txt:
+// N = 32, 64, 128: 67 cycles; N = 256: 128), so the MMA N must be large: a
+// tile is 24 nodes = 96 (node, direction) columns, the largest N whose
+// operands fit beside the table.
+//
+// Per CTA:
+//   tensor memory  columns [0, 96) and [128, 224): two accumulator stages
+//                  [128 labels x 96 columns] fp32;
+//                  Ms = 128: [256, 384) f_hi and [384, 512) f_lo rows of the table
+//                  (both A operands from tensor memory, no shared-memory A reads);
+//                  Ms = 256: [256, 512) f_lo, f_hi in shared memory
+//   shared memory  Ms = 256: f_hi rows of this CTA [128 x 256] tf32, K-major,
+//                  128-byte swizzle (128 KB);
+//                  a ring of 48 KB slots, each one K-half (Ms/2 labels) of this
+//                  CTA's columns of a tile, hi and lo planes, K-major swizzled
+//                  (Ms = 128: 4 slots, Ms = 256: 2 slots)
+// Warp roles (17 warps, one CTA per SM, persistent over tiles):
 //   warps 0-3    epilogue: tcgen05.ld the accumulator (thread = output label),
 //                scale by the column's 1/s, store into the neighbour's slot
 //                (a warp stores 128 contiguous bytes per column)
-//   warp 4       allocates tensor memory; one elected thread of the leader CTA
-//                issues the 3 Ms/8 tcgen05.mma of a tile and commits to an mbarrier
-//   warps 5-16   producers, 3 groups of 4 warps, group g fills stage g: read the
-//                unary and the four incoming messages of the tile's nodes once,
-//                form the four exclusion products in the reference order, split
-//                hi / lo straight into the swizzled operand rows, and compute the
-//                normaliser s = sum_{x_j} colsum_f(x_j) h(x_j) (equal to the sum of
-//                the outputs up to rounding; the reference divides by that sum)
-// mbarriers per stage: full (producers -> MMA), accf (MMA commit -> epilogue),
-// invf (producers -> epilogue: the 1/s values), free (epilogue -> producers).
+//   warp 4       allocates tensor memory; one thread of the leader CTA issues
+//                the tcgen05.mma of each K-half (3 products x Ms/16) and commits
+//                to the slot's `empty` mbarrier (and the accumulator's `accf`)
+//   warps 5-16   producers, one pass per tile each: read the unary and the four
+//                incoming messages of their node(s) once, form the four
+//                exclusion products in the reference order, split hi / lo
+//                straight into the swizzled operand rows of the two K-half
+//                slots, and compute the normaliser s = sum_{x_j} colsum_f(x_j)
+//                h(x_j) (equal to the sum of the outputs up to rounding; the
+//                reference divides by that sum).  The next tile's inputs are
+//                loaded as soon as the products are formed, and prefetched into
+//                L2 two tiles ahead.
+// mbarriers: full[slot] (producers -> MMA), empty[slot] (MMA commit -> producers),
+// accf[stage] (MMA commit -> epilogue), accfree[stage] (epilogue -> MMA),
+// invf[tile % 4] (producers -> epilogue: the 1/s values).
 #include "aux_kernels.cuh"
 #include "band_kernel.cuh"   // vmul, lanes_sum, smem_u32, mbar_init
 
 namespace sbp {
 namespace tc {
 
-constexpr int TC_NODES = 8;                 // nodes per tile
-constexpr int TC_N = 4 * TC_NODES;          // MMA N: (node, direction) columns per tile
-constexpr int TC_STAGES = 3;
+constexpr int TC_NODES = 24;                // nodes per tile
+constexpr int TC_N = 4 * TC_NODES;          // MMA N = 96: (node, direction) columns per tile
 constexpr int TC_EPI_WARPS = 4;
-constexpr int TC_PROD_WARPS = 4 * TC_STAGES;
+constexpr int TC_PROD_WARPS = 12;
 constexpr int TC_WARPS = TC_EPI_WARPS + 1 + TC_PROD_WARPS;
 constexpr int TC_THREADS = 32 * TC_WARPS;   // 544
-constexpr int TC_ACOL = 128;                // tensor-memory column of f_lo
+constexpr int TC_ACC = 2;                   // accumulator stages, 128 tensor-memory columns apart
+constexpr int TC_ACOL = 256;                // first tensor-memory column of the table operand(s)
+constexpr int TC_TCOLS = 512;
+constexpr int TC_INV = 4;                   // ring of per-tile 1/s vectors
 
 template <int MS>
 struct TcShape {
     static constexpr int CG = MS / 128;               // CTAs per MMA (cta_group)
-    static constexpr int NB = TC_N / CG;              // h-tile columns held by one CTA
-    static constexpr int KA = MS / 32;                // 128-byte swizzle atoms along K
-    static constexpr int A_ATOM = 128 * 128;          // bytes: 128 rows x 32 tf32
-    static constexpr int B_ATOM = NB * 128;
-    static constexpr int A_BYTES = KA * A_ATOM;
-    static constexpr int B_PLANE = KA * B_ATOM;
-    static constexpr int STAGE_BYTES = 2 * B_PLANE;   // hi and lo planes
+    static constexpr int NB = TC_N / CG;              // tile columns (B rows) held by one CTA
+    static constexpr int NCTA = TC_NODES / CG;        // nodes of a tile formed by one CTA
     static constexpr int LP = MS / 8;                 // lanes per node (8 labels each)
     static constexpr int NPW = 32 / LP;               // nodes per producer warp
-    static constexpr int NCTA = TC_NODES / CG;        // nodes of a tile formed by one CTA
-    static constexpr int TCOLS = MS == 128 ? 256 : 512;
-    static constexpr int AUX_BYTES = 2048;            // colsum, 1/s, mbarriers, tmem address
-    static constexpr size_t SMEM = (size_t)A_BYTES + TC_STAGES * STAGE_BYTES + AUX_BYTES;
+    static constexpr int KH = MS / 2;                 // labels per K-half
+    static constexpr int KSTEPS = KH / 8;             // MMAs (K = 8) per product and K-half
+    static constexpr int B_ATOM = NB * 128;           // bytes: NB rows x 32 tf32
+    static constexpr int B_PLANE = (KH / 32) * B_ATOM;
+    static constexpr int SLOT_BYTES = 2 * B_PLANE;    // hi and lo planes: 48 KB
+    static constexpr int NSLOT = MS == 128 ? 4 : 2;
+    static constexpr bool A_HI_SMEM = MS == 256;      // f_hi in shared memory (no room in tensor memory)
+    static constexpr int A_ATOM = 128 * 128;          // bytes: 128 rows x 32 tf32
+    static constexpr int A_BYTES = A_HI_SMEM ? (MS / 32) * A_ATOM : 0;
+    static constexpr int ACOL_HI = TC_ACOL;           // Ms = 128 only
+    static constexpr int ACOL_LO = MS == 128 ? TC_ACOL + 128 : TC_ACOL;
+    static constexpr int AUX_BYTES = 3072;            // colsum, 1/s ring, mbarriers, tmem address
+    static constexpr size_t SMEM = (size_t)A_BYTES + NSLOT * SLOT_BYTES + AUX_BYTES;
     static_assert(MS == 128 || MS == 256, "tensor-core dense kernel: Ms = 128 or 256");
-    static_assert(NPW * 4 == NCTA, "four producer warps form one CTA's share of a tile");
+    static_assert(NPW * TC_PROD_WARPS == NCTA, "every producer warp forms its node(s) of every tile");
+    static_assert(SLOT_BYTES == 49152 && SMEM <= 232448, "shared-memory budget");
 };
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -90,8 +114,10 @@ __device__ __forceinline__ void bar_arrive(unsigned long long *bar, unsigned ran
                          mapa(smem_u32(bar), rank)) : "memory");
 }
 
-// Bounded spin: a protocol error traps instead of hanging the device.
-template <int CG>
+// Bounded spin: a protocol error traps instead of hanging the device.  SLEEP
+// (ns) backs the producers' polling off so it does not take issue slots from
+// the warps that work.
+template <int CG, int SLEEP>
 __device__ __forceinline__ void bar_wait(unsigned long long *bar, unsigned parity) {
     unsigned done = 0;
     for (unsigned spin = 0; !done; ++spin) {
@@ -101,8 +127,14 @@ __device__ __forceinline__ void bar_wait(unsigned long long *bar, unsigned parit
         else
             asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
                          " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-        if (spin > (1u << 27)) __trap();
+        if (!done && SLEEP > 0) __nanosleep(SLEEP);
+        if (spin > (1u << 26)) __trap();
     }
+}
+
+__device__ __forceinline__ void st_global_if(float *p, float v, bool pred) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.global.f32 [%0], %1;\n}" ::"l"(p), "f"(v),
+                 "r"((int)pred) : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -216,14 +248,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     using S = TcShape<MS>;
     constexpr int CG = S::CG;
     extern __shared__ __align__(1024) unsigned char tc_smem[];
-    unsigned char *sA = tc_smem;
-    unsigned char *sB = tc_smem + S::A_BYTES;
-    float *csum = reinterpret_cast<float *>(sB + TC_STAGES * S::STAGE_BYTES);   // [MS]
-    float *inv = csum + MS;                                                     // [stage][32]
-    unsigned long long *bars = reinterpret_cast<unsigned long long *>(inv + TC_STAGES * TC_N);
-    unsigned long long *full = bars, *accf = bars + TC_STAGES, *invf = bars + 2 * TC_STAGES,
-                       *freeb = bars + 3 * TC_STAGES;
-    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 4 * TC_STAGES);
+    unsigned char *sA = tc_smem;                       // Ms = 256: f_hi
+    unsigned char *sB = tc_smem + S::A_BYTES;          // slot ring
+    float *csum = reinterpret_cast<float *>(sB + S::NSLOT * S::SLOT_BYTES);   // [MS]
+    float *inv = csum + MS;                                                   // [TC_INV][TC_N]
+    unsigned long long *bars = reinterpret_cast<unsigned long long *>(inv + TC_INV * TC_N);
+    unsigned long long *full = bars, *empty = bars + 4, *accf = bars + 8, *accfree = bars + 10,
+                       *invf = bars + 12;
+    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 16);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned rank = CG == 2 ? cluster_rank() : 0u;
@@ -232,17 +264,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     const long long tiles = (npix + TC_NODES - 1) / TC_NODES;
     const float *tab = a.t[0];
 
-    // ---- one-time setup: f_hi -> shared memory, column sums, barriers, tensor memory
-    for (int i = tid; i < 128 * (MS / 4); i += TC_THREADS) {
-        const int row = i / (MS / 4), ch = i % (MS / 4);
-        const float4 v = *reinterpret_cast<const float4 *>(tab + (size_t)(128 * rank + row) * MS + 4 * ch);
-        sts128(smem_u32(sA) + sw128_chunk(row, ch, S::A_ATOM), tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z),
-               tf32_rna(v.w));
+    // ---- one-time setup: table operands, column sums, barriers, tensor memory
+    if (S::A_HI_SMEM) {
+        for (int i = tid; i < 128 * (MS / 4); i += TC_THREADS) {
+            const int row = i / (MS / 4), ch = i % (MS / 4);
+            const float4 v = *reinterpret_cast<const float4 *>(tab + (size_t)(128 * rank + row) * MS + 4 * ch);
+            sts128(smem_u32(sA) + sw128_chunk(row, ch, S::A_ATOM), tf32_rna(v.x), tf32_rna(v.y),
+                   tf32_rna(v.z), tf32_rna(v.w));
+        }
     }
     {
         // column sums of the whole table, fixed order: SL row slices, then the slices
         constexpr int SL = 2;
-        float *part = reinterpret_cast<float *>(sB);   // [SL][MS] scratch in stage 0
+        float *part = reinterpret_cast<float *>(sB);   // [SL][MS] scratch in slot 0
         if (tid < SL * MS) {
             const int x = tid % MS, sl = tid / MS;
             float s = 0.0f;
@@ -258,22 +292,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
         }
     }
     if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
-            mbar_init(&full[s], 4 * CG);
-            mbar_init(&accf[s], 1);
-            mbar_init(&invf[s], 4 * CG);
-            mbar_init(&freeb[s], TC_EPI_WARPS * CG);
+        for (int s = 0; s < S::NSLOT; ++s) {
+            mbar_init(&full[s], TC_PROD_WARPS * CG);
+            mbar_init(&empty[s], 1);
         }
+        for (int s = 0; s < TC_ACC; ++s) {
+            mbar_init(&accf[s], 1);
+            mbar_init(&accfree[s], TC_EPI_WARPS * CG);
+        }
+        for (int s = 0; s < TC_INV; ++s) mbar_init(&invf[s], TC_PROD_WARPS * CG);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == TC_EPI_WARPS) {
         if (CG == 1) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             smem_u32(tmem_slot)), "n"(S::TCOLS) : "memory");
+                             smem_u32(tmem_slot)), "n"(TC_TCOLS) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         } else {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             smem_u32(tmem_slot)), "n"(S::TCOLS) : "memory");
+                             smem_u32(tmem_slot)), "n"(TC_TCOLS) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
         }
     }
@@ -282,19 +319,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     tc_fence_after();
     const unsigned tmem = *tmem_slot;
     if (warp < TC_EPI_WARPS) {
-        // f_lo rows of this CTA -> tensor memory: lane = label row, column = k
+        // table rows of this CTA -> tensor memory: lane = label row, column = k
         const float *row = tab + (size_t)(128 * rank + 32 * warp + lane) * MS;
+        const unsigned lane_base = tmem + ((unsigned)(32 * warp) << 16);
         for (int k0 = 0; k0 < MS; k0 += 32) {
-            float v[32];
+            float hi[32], lo[32];
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
                 const float4 t = *reinterpret_cast<const float4 *>(row + k0 + i);
-                v[i] = t.x - tf32_rna(t.x);
-                v[i + 1] = t.y - tf32_rna(t.y);
-                v[i + 2] = t.z - tf32_rna(t.z);
-                v[i + 3] = t.w - tf32_rna(t.w);
+                hi[i] = tf32_rna(t.x); hi[i + 1] = tf32_rna(t.y);
+                hi[i + 2] = tf32_rna(t.z); hi[i + 3] = tf32_rna(t.w);
+                lo[i] = t.x - hi[i]; lo[i + 1] = t.y - hi[i + 1];
+                lo[i + 2] = t.z - hi[i + 2]; lo[i + 3] = t.w - hi[i + 3];
             }
-            tmem_st32(tmem + ((unsigned)(32 * warp) << 16) + TC_ACOL + k0, v);
+            if (!S::A_HI_SMEM) tmem_st32(lane_base + S::ACOL_HI + k0, hi);
+            tmem_st32(lane_base + S::ACOL_LO + k0, lo);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -309,40 +348,50 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
 
     if (warp < TC_EPI_WARPS) {
         // ================= epilogue =================
-        const int x = 128 * (int)rank + 32 * warp + lane;   // output label of this thread
+        // Thread = output label x; column n = (node, direction).  The four
+        // destinations of a node are fixed offsets from the node's own slot-0
+        // address, and consecutive nodes of a tile are consecutive in memory.
+        const int x = 128 * (int)rank + 32 * warp + lane;
         const long long W = a.W;
+        float *const d0 = a.msgs_out + x + dir_wslot(0) * a.slot_stride + a.Ms;       // right neighbour
+        float *const d1 = a.msgs_out + x + dir_wslot(1) * a.slot_stride - a.Ms;       // left
+        float *const d2 = a.msgs_out + x + dir_wslot(2) * a.slot_stride + W * a.Ms;   // below
+        float *const d3 = a.msgs_out + x + dir_wslot(3) * a.slot_stride - W * a.Ms;   // above
         long long i = 0;
         for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
-            const int s = (int)(i % TC_STAGES);
-            const unsigned par = (unsigned)((i / TC_STAGES) & 1);
-            bar_wait<CG>(&invf[s], par);
-            bar_wait<CG>(&accf[s], par);
+            const int acc = (int)(i % TC_ACC), ir = (int)(i % TC_INV);
+            bar_wait<CG, 0>(&invf[ir], (unsigned)((i / TC_INV) & 1));
+            bar_wait<CG, 0>(&accf[acc], (unsigned)((i / TC_ACC) & 1));
             tc_fence_after();
-            float v[32];
-            tmem_ld32(tmem + ((unsigned)(32 * warp) << 16) + TC_N * s, v);
-            const float *iv = inv + s * TC_N;
+            const float4 *iv4 = reinterpret_cast<const float4 *>(inv + ir * TC_N);
             const long long p0 = tile * TC_NODES;
             int lr = a.lr_begin + (int)(p0 / W);
             int c = (int)(p0 % W);
+            long long off = ((long long)lr * W + c) * a.Ms;   // node's element offset in a slot plane
+            long long left = npix - p0;                        // nodes of the strip from p0 on
+#pragma unroll 1
+            for (int cc = 0; cc < TC_N / 32; ++cc) {
+                float v[32];
+                float4 s4[8];
 #pragma unroll
-            for (int n = 0; n < TC_NODES; ++n) {
-                if (p0 + n < npix) {
+                for (int n = 0; n < 8; ++n) s4[n] = iv4[8 * cc + n];   // the 1/s of 8 nodes (broadcast reads)
+                tmem_ld32(tmem + ((unsigned)(32 * warp) << 16) + 128 * acc + 32 * cc, v);
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    const bool in = left > 0;
                     const long long r = (long long)a.r0 + lr - 1;
-                    const long long node_l = (long long)lr * W + c;
-                    float *base = a.msgs_out + node_l * a.Ms + x;
-                    if (c + 1 < a.W) base[dir_wslot(0) * a.slot_stride + a.Ms] = v[4 * n + 0] * iv[4 * n + 0];
-                    if (c > 0) base[dir_wslot(1) * a.slot_stride - a.Ms] = v[4 * n + 1] * iv[4 * n + 1];
-                    if (r + 1 < a.H) base[dir_wslot(2) * a.slot_stride + W * a.Ms] = v[4 * n + 2] * iv[4 * n + 2];
-                    if (r > 0) base[dir_wslot(3) * a.slot_stride - W * a.Ms] = v[4 * n + 3] * iv[4 * n + 3];
+                    st_global_if(d0 + off, v[4 * n + 0] * s4[n].x, in && c + 1 < a.W);
+                    st_global_if(d1 + off, v[4 * n + 1] * s4[n].y, in && c > 0);
+                    st_global_if(d2 + off, v[4 * n + 2] * s4[n].z, in && r + 1 < a.H);
+                    st_global_if(d3 + off, v[4 * n + 3] * s4[n].w, in && r > 0);
+                    off += a.Ms;
+                    --left;
+                    if (++c == a.W) { c = 0; ++lr; }
                 }
-                if (++c == a.W) { c = 0; ++lr; }
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                bar_arrive<CG>(&freeb[s], rank);
-                if (CG == 2) bar_arrive<CG>(&freeb[s], rank ^ 1u);
-            }
+            if (lane == 0) bar_arrive<CG>(&accfree[acc], 0u);   // the leader's MMA thread waits on it
         }
     } else if (warp == TC_EPI_WARPS) {
         // ================= MMA issuer (leader CTA) =================
@@ -352,102 +401,121 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             const unsigned sA_u = smem_u32(sA), sB_u = smem_u32(sB);
             long long i = 0;
             for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
-                const int s = (int)(i % TC_STAGES);
-                const unsigned par = (unsigned)((i / TC_STAGES) & 1);
-                bar_wait<CG>(&full[s], par);
-                tc_fence_after();
-                if (lane == 0) {
-                    const unsigned d = tmem + TC_N * s;
-                    const unsigned bhi = sB_u + s * S::STAGE_BYTES, blo = bhi + S::B_PLANE;
-                    // f_hi h_lo, f_lo h_hi (small terms first), then f_hi h_hi
+                const int acc = (int)(i % TC_ACC);
+                bar_wait<CG, 0>(&accfree[acc], (unsigned)(((i / TC_ACC) & 1) ^ 1));
+                const unsigned d = tmem + 128 * acc;
+#pragma unroll 1
+                for (int hh = 0; hh < 2; ++hh) {
+                    const long long q = 2 * i + hh;
+                    const int slot = (int)(q % S::NSLOT);
+                    bar_wait<CG, 0>(&full[slot], (unsigned)((q / S::NSLOT) & 1));
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const unsigned bhi = sB_u + slot * S::SLOT_BYTES, blo = bhi + S::B_PLANE;
+                        // f_hi h_lo, f_lo h_hi (small terms first), then f_hi h_hi
 #pragma unroll 4
-                    for (int k = 0; k < MS / 8; ++k)
-                        mma_ss<CG>(d, sw128_desc(sA_u + (k >> 2) * S::A_ATOM + (k & 3) * 32),
-                                   sw128_desc(blo + (k >> 2) * S::B_ATOM + (k & 3) * 32), idesc, k > 0);
+                        for (int k = 0; k < S::KSTEPS; ++k) {
+                            const int kk = hh * S::KSTEPS + k;
+                            const unsigned long long bd = sw128_desc(blo + (k >> 2) * S::B_ATOM + (k & 3) * 32);
+                            if (S::A_HI_SMEM)
+                                mma_ss<CG>(d, sw128_desc(sA_u + (kk >> 2) * S::A_ATOM + (kk & 3) * 32), bd, idesc,
+                                           (hh | k) > 0);
+                            else
+                                mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, (hh | k) > 0);
+                        }
 #pragma unroll 4
-                    for (int k = 0; k < MS / 8; ++k)
-                        mma_ts<CG>(d, tmem + TC_ACOL + 8 * k,
-                                   sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32), idesc, 1u);
+                        for (int k = 0; k < S::KSTEPS; ++k) {
+                            const int kk = hh * S::KSTEPS + k;
+                            mma_ts<CG>(d, tmem + S::ACOL_LO + 8 * kk,
+                                       sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32), idesc, 1u);
+                        }
 #pragma unroll 4
-                    for (int k = 0; k < MS / 8; ++k)
-                        mma_ss<CG>(d, sw128_desc(sA_u + (k >> 2) * S::A_ATOM + (k & 3) * 32),
-                                   sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32), idesc, 1u);
-                    mma_commit<CG>(&accf[s]);
+                        for (int k = 0; k < S::KSTEPS; ++k) {
+                            const int kk = hh * S::KSTEPS + k;
+                            const unsigned long long bd = sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32);
+                            if (S::A_HI_SMEM)
+                                mma_ss<CG>(d, sw128_desc(sA_u + (kk >> 2) * S::A_ATOM + (kk & 3) * 32), bd, idesc, 1u);
+                            else
+                                mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, 1u);
+                        }
+                        mma_commit<CG>(&empty[slot]);          // the slot is free once these complete
+                        if (hh == 1) mma_commit<CG>(&accf[acc]);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
     } else {
         // ================= producers =================
         constexpr int LP = S::LP, NPW = S::NPW;
         const int pw = warp - TC_EPI_WARPS - 1;
-        const int grp = pw / 4, wq = pw % 4;
         const int j = lane % LP, q = lane / LP;
-        const int nl = wq * NPW + q;                       // node within this CTA's share of the tile
-        const int ch0 = j, ch1 = j + LP;                   // this lane's two 4-label chunks
-        float cs[8];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            cs[u] = csum[4 * ch0 + u];
-            cs[4 + u] = csum[4 * ch1 + u];
-        }
-        const unsigned stage_u = smem_u32(sB) + grp * S::STAGE_BYTES;
-        float *iv = inv + grp * TC_N;
-        const unsigned iv_remote = CG == 2 ? mapa(smem_u32(iv), rank ^ 1u) : 0u;
-        long long i = grp;
-        for (long long tile = cluster + grp * nclusters; tile < tiles;
-             tile += TC_STAGES * nclusters, i += TC_STAGES) {
-            const long long p0 = tile * TC_NODES;
-            if (wq == 0 && lane < 5) {
-                // the group's next tile: into L2 while this one is formed
-                const long long np0 = p0 + (long long)TC_STAGES * nclusters * TC_NODES;
-                if (np0 < npix && !(lane < 4 && a.first)) {
-                    const long long n = npix - np0 < TC_NODES ? npix - np0 : TC_NODES;
-                    const float *src = lane == 4
-                        ? a.values + ((long long)(a.lr_begin - 1) * a.W + np0) * a.Ms
-                        : a.msgs_in + lane * a.slot_stride + ((long long)a.lr_begin * a.W + np0) * a.Ms;
-                    l2_prefetch(src, (unsigned)(n * a.Ms * 4));
-                }
-            }
-            long long p = p0 + (long long)rank * S::NCTA + nl;
-            const bool valid = p < npix;
+        const int nl = pw * NPW + q;                       // node within this CTA's share of the tile
+        const unsigned sB_u = smem_u32(sB);
+        float g[8], m[4][8];
+        long long p, node_l, r;
+        int c;
+        bool valid;
+        auto locate = [&](long long tile) {
+            p = tile * TC_NODES + (long long)rank * S::NCTA + nl;
+            valid = p < npix;
             if (!valid) p = npix - 1;
             const int lr = a.lr_begin + (int)(p / a.W);
-            const int c = (int)(p % a.W);
-            const long long r = (long long)a.r0 + lr - 1;
-            const long long node_l = (long long)lr * a.W + c;
-            float g[8], m[4][8];
-            {
-                const float *gp = a.values + ((long long)(lr - 1) * a.W + c) * a.Ms;
-                const float4 g0 = ldg_stream(reinterpret_cast<const float4 *>(gp + 4 * ch0));
-                const float4 g1 = ldg_stream(reinterpret_cast<const float4 *>(gp + 4 * ch1));
-                g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w;
-                g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
-                if (!a.first) {
-                    const float *mp = a.msgs_in + node_l * a.Ms;
+            c = (int)(p % a.W);
+            r = (long long)a.r0 + lr - 1;
+            node_l = (long long)lr * a.W + c;
+        };
+        auto load = [&]() {
+            const float *gp = a.values + (node_l - a.W) * a.Ms;   // values row lr - 1
+            const float4 g0 = ldg_stream(reinterpret_cast<const float4 *>(gp + 4 * j));
+            const float4 g1 = ldg_stream(reinterpret_cast<const float4 *>(gp + S::KH + 4 * j));
+            g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w;
+            g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+            if (!a.first) {
+                const float *mp = a.msgs_in + node_l * a.Ms;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float4 m0 = ldg_stream(reinterpret_cast<const float4 *>(mp + k * a.slot_stride + 4 * ch0));
-                        const float4 m1 = ldg_stream(reinterpret_cast<const float4 *>(mp + k * a.slot_stride + 4 * ch1));
-                        m[k][0] = m0.x; m[k][1] = m0.y; m[k][2] = m0.z; m[k][3] = m0.w;
-                        m[k][4] = m1.x; m[k][5] = m1.y; m[k][6] = m1.z; m[k][7] = m1.w;
-                    }
-                } else {
-                    // bp.py:587-601 without touching memory
-                    const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
+                for (int k = 0; k < 4; ++k) {
+                    const float4 m0 = ldg_stream(reinterpret_cast<const float4 *>(mp + k * a.slot_stride + 4 * j));
+                    const float4 m1 = ldg_stream(reinterpret_cast<const float4 *>(mp + k * a.slot_stride + S::KH + 4 * j));
+                    m[k][0] = m0.x; m[k][1] = m0.y; m[k][2] = m0.z; m[k][3] = m0.w;
+                    m[k][4] = m1.x; m[k][5] = m1.y; m[k][6] = m1.z; m[k][7] = m1.w;
+                }
+            } else {
+                // bp.py:587-601 without touching memory
+                const bool ghost[4] = {r == 0, c == 0, c == a.W - 1, r == a.H - 1};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float real = ghost[k] ? 1.0f : 1.0f / (float)a.M;
+                for (int k = 0; k < 4; ++k) {
+                    const float real = ghost[k] ? 1.0f : 1.0f / (float)a.M;
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int xx = u < 4 ? 4 * ch0 + u : 4 * ch1 + (u - 4);
-                            m[k][u] = xx < a.M ? real : 0.0f;
-                        }
+                    for (int u = 0; u < 8; ++u) {
+                        const int xx = u < 4 ? 4 * j + u : S::KH + 4 * j + (u - 4);
+                        m[k][u] = xx < a.M ? real : 0.0f;
                     }
                 }
             }
-            // the stage is free once the epilogue of the tile that used it is done
-            bar_wait<CG>(&freeb[grp], (unsigned)(((i / TC_STAGES) & 1) ^ 1));
+        };
+        auto prefetch = [&](long long tile) {
+            // one warp of the CTA: the tile's five contiguous input spans into L2
+            if (pw != 0 || lane >= 5 || tile >= tiles || (lane < 4 && a.first)) return;
+            const long long q0 = tile * TC_NODES + (long long)rank * S::NCTA;
+            if (q0 >= npix) return;
+            const long long n = npix - q0 < S::NCTA ? npix - q0 : S::NCTA;
+            const float *src = lane == 4
+                ? a.values + ((long long)(a.lr_begin - 1) * a.W + q0) * a.Ms
+                : a.msgs_in + lane * a.slot_stride + ((long long)a.lr_begin * a.W + q0) * a.Ms;
+            l2_prefetch(src, (unsigned)(n * a.Ms * 4));
+        };
+        if (cluster < tiles) {
+            locate(cluster);
+            load();
+            prefetch(cluster + nclusters);
+        }
+        long long i = 0;
+        for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
+            prefetch(tile + 2 * nclusters);
+            const long long r_cur = r;
+            const int c_cur = c;
+            const bool valid_cur = valid;
             const bool has[4] = {c + 1 < a.W, c > 0, r + 1 < a.H, r > 0};
             // exclusion products in the reference order (unary, then slots 0..3
             // ascending, skipping the excluded one; prefixes shared)
@@ -461,40 +529,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             vmul(ab, ab, m[1]);
             vmul(h[0], ab, m[3]);         // excl 2 -> dir 0
             vmul(h[2], ab, m[2]);         // excl 3 -> dir 2
-#pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                const int row = nl * 4 + d;                // column of this CTA's h tile
-                float hi[8], lo[8], sd = 0.0f;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    hi[u] = tf32_rna(h[d][u]);
-                    lo[u] = h[d][u] - hi[u];
-                    sd = fmaf(cs[u], h[d][u], sd);
-                }
-                const unsigned o0 = stage_u + sw128_chunk(row, ch0, S::B_ATOM);
-                const unsigned o1 = stage_u + sw128_chunk(row, ch1, S::B_ATOM);
-                sts128(o0, hi[0], hi[1], hi[2], hi[3]);
-                sts128(o1, hi[4], hi[5], hi[6], hi[7]);
-                sts128(o0 + S::B_PLANE, lo[0], lo[1], lo[2], lo[3]);
-                sts128(o1 + S::B_PLANE, lo[4], lo[5], lo[6], lo[7]);
-                sd = lanes_sum<LP>(sd);
-                if (j == 0) {
-                    const float rs = __frcp_rn(sd);
-                    const int col = ((int)rank * S::NCTA + nl) * 4 + d;
-                    iv[col] = rs;
-                    if (CG == 2)
-                        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(iv_remote + 4 * col), "f"(rs) : "memory");
-                    const bool ok = (sd > 0.0f) && !isinf(sd);
-                    if (!ok && valid && has[d])
-                        report_failure(a.err, a.iteration, directed_edge_id(a.H, a.W, r, c, d));
-                }
+            // the inputs are dead: fetch the next tile's while this one is split and stored
+            if (tile + nclusters < tiles) {
+                locate(tile + nclusters);
+                load();
             }
-            asm volatile("fence.proxy.async;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                bar_arrive<CG>(&full[grp], 0u);
-                bar_arrive<CG>(&invf[grp], rank);
-                if (CG == 2) bar_arrive<CG>(&invf[grp], rank ^ 1u);
+            float sd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const long long qq = 2 * i + hh;
+                const int slot = (int)(qq % S::NSLOT);
+                bar_wait<CG, 64>(&empty[slot], (unsigned)(((qq / S::NSLOT) & 1) ^ 1));
+                const unsigned slot_u = sB_u + slot * S::SLOT_BYTES;
+                const float4 cs4 = *reinterpret_cast<const float4 *>(csum + hh * S::KH + 4 * j);
+                const float cs[4] = {cs4.x, cs4.y, cs4.z, cs4.w};
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const int row = nl * 4 + d;            // column of this CTA's share of the tile
+                    float hi[4], lo[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float hv = h[d][4 * hh + u];
+                        hi[u] = tf32_rna(hv);
+                        lo[u] = hv - hi[u];
+                        sd[d] = fmaf(cs[u], hv, sd[d]);
+                    }
+                    const unsigned o = slot_u + sw128_chunk(row, j, S::B_ATOM);
+                    sts128(o, hi[0], hi[1], hi[2], hi[3]);
+                    sts128(o + S::B_PLANE, lo[0], lo[1], lo[2], lo[3]);
+                }
+                if (hh == 1) {
+                    // 1/s of the node's four messages, before the slot is published
+                    const int ir = (int)(i % TC_INV);
+                    float *iv = inv + ir * TC_N;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const float s = lanes_sum<LP>(sd[d]);
+                        if (j == 0) {
+                            const float rs = __frcp_rn(s);
+                            const int col = ((int)rank * S::NCTA + nl) * 4 + d;
+                            iv[col] = rs;
+                            if (CG == 2)
+                                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
+                                                 mapa(smem_u32(iv + col), rank ^ 1u)), "f"(rs) : "memory");
+                            const bool ok = (s > 0.0f) && !isinf(s);
+                            if (!ok && valid_cur && has[d])
+                                report_failure(a.err, a.iteration, directed_edge_id(a.H, a.W, r_cur, c_cur, d));
+                        }
+                    }
+                }
+                // this thread's operand rows (generic proxy, own shared memory) -> tensor-core reads
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    bar_arrive<CG>(&full[slot], 0u);
+                    if (hh == 1) {
+                        const int ir = (int)(i % TC_INV);
+                        bar_arrive<CG>(&invf[ir], rank);
+                        if (CG == 2) bar_arrive<CG>(&invf[ir], rank ^ 1u);
+                    }
+                }
             }
         }
     }
@@ -508,9 +602,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     }
     if (warp == TC_EPI_WARPS) {
         if (CG == 1)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(S::TCOLS) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TCOLS) : "memory");
         else
-            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(S::TCOLS) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TCOLS) : "memory");
     }
 }
 

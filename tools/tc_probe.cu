@@ -246,6 +246,98 @@ static int run(const char *name) {
     return bad || hS[0] || hS[1];
 }
 
+
+// ---- MMA issue-rate benchmark: REP back-to-back tcgen05.mma (kind::tf32, K = 8)
+// of shape (128 CG) x NN, A from shared memory (SS) or tensor memory (TS);
+// cycles per MMA from clock64 around issue + commit + wait.
+template <int CG, bool ATMEM, int NN>
+__global__ void __launch_bounds__(128) mma_rate(long long *cycles, int rep) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ unsigned tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    unsigned rank = 0;
+    if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    constexpr int NB = NN / CG;
+    constexpr int A_ATOM = 128 * 128, B_ATOM = NB * 128;
+    unsigned char *sA = smem, *sB = smem + 4 * A_ATOM;
+    for (int i = tid; i < (4 * A_ATOM + 4 * B_ATOM) / 4; i += 128) ((float *)smem)[i] = 0.0f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        if (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(512) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(512) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (CG == 2) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base_s;
+    long long t0 = 0;
+    if (tid == 0 && rank == 0) {
+        const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(NN >> 3) << 17) |
+                               ((unsigned)((128 * CG) >> 4) << 24);
+        t0 = clock64();
+        for (int r = 0; r < rep; ++r) {
+            const int k = r & 15, ka = k >> 2, ks = k & 3;
+            const unsigned long long bd = sw128_desc(smem_u32(sB) + ka * B_ATOM + ks * 32);
+            if (ATMEM) mma_ts<CG>(tmem, tmem + 256 + 8 * k, bd, idesc, 1u);
+            else mma_ss<CG>(tmem, sw128_desc(smem_u32(sA) + ka * A_ATOM + ks * 32), bd, idesc, 1u);
+        }
+        if (CG == 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "h"((unsigned short)3) : "memory");
+    }
+    mbar_wait(&bar, 0);
+    if (tid == 0 && rank == 0) cycles[0] = clock64() - t0;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (CG == 2) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (warp == 0) {
+        if (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+    }
+}
+
+template <int CG, bool ATMEM, int NN>
+static void rate(const char *name) {
+    long long *d, h = 0;
+    CK(cudaMalloc(&d, 8));
+    const size_t smem = 4 * 128 * 128 + 4 * (NN / CG) * 128;
+    CK(cudaFuncSetAttribute(mma_rate<CG, ATMEM, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CG); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    const int rep = 4096;
+    for (int it = 0; it < 2; ++it) {
+        CK(cudaLaunchKernelEx(&cfg, mma_rate<CG, ATMEM, NN>, d, rep));
+        CK(cudaDeviceSynchronize());
+    }
+    CK(cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost));
+    printf("rate %s N=%d: %.1f cycles per MMA (floor %d)\n", name, NN, (double)h / rep, 128 * NN / 256);
+    cudaFree(d);
+}
+
 int main(int argc, char **argv) {
     const int mode = argc > 1 ? atoi(argv[1]) : -1;
     int rc = 0;
@@ -253,5 +345,11 @@ int main(int argc, char **argv) {
     if (mode < 0 || mode == 1) rc |= run<1, true>("mode1 cg1 TS");
     if (mode < 0 || mode == 2) rc |= run<2, false>("mode2 cg2 SS");
     if (mode < 0 || mode == 3) rc |= run<2, true>("mode3 cg2 TS");
+    if (mode == 9) {
+        rate<1, false, 32>("cg1 SS"); rate<1, false, 64>("cg1 SS"); rate<1, false, 128>("cg1 SS"); rate<1, false, 256>("cg1 SS");
+        rate<1, true, 32>("cg1 TS"); rate<1, true, 64>("cg1 TS"); rate<1, true, 128>("cg1 TS"); rate<1, true, 256>("cg1 TS");
+        rate<2, false, 32>("cg2 SS"); rate<2, false, 64>("cg2 SS"); rate<2, false, 128>("cg2 SS"); rate<2, false, 256>("cg2 SS");
+        rate<2, true, 32>("cg2 TS"); rate<2, true, 64>("cg2 TS"); rate<2, true, 128>("cg2 TS"); rate<2, true, 256>("cg2 TS");
+    }
     return rc;
 }
