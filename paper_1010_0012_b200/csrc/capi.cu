@@ -302,7 +302,8 @@ int kernel_radius(int Ms, int R, int domain) {
 // SAME device pointer for both orientations -- and Ms is 128 or 256.
 bool dense_on_tensor_cores(const sbp_grid *g, const sbp_potential *pot) {
     return knobs().dense_tc != 0 && pot->domain == SBP_SUM && pot->n_pot == 0 &&
-           pot->dense_t[0] && pot->dense_t[0] == pot->dense_t[1] && sbp::dense_tc_supported(g->Ms);
+           pot->dense_t[0] && pot->dense_t[0] == pot->dense_t[1] && sbp::dense_tc_supported(g->Ms) &&
+           (long long)g->rows * g->W < (1ll << 31);
 }
 
 int band_radius(const sbp_grid *g, const sbp_potential *pot) {

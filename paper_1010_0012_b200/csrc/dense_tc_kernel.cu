@@ -29,22 +29,22 @@
 //                  a ring of 48 KB slots, each one K-half (Ms/2 labels) of this
 //                  CTA's columns of a tile, hi and lo planes, K-major swizzled
 //                  (Ms = 128: 4 slots, Ms = 256: 2 slots)
-// Warp roles (17 warps, one CTA per SM, persistent over tiles):
+// Warp roles (20 warps, one CTA per SM, persistent over tiles):
 //   warps 0-3    epilogue: tcgen05.ld the accumulator (thread = output label),
 //                scale by the column's 1/s, store into the neighbour's slot
 //                (a warp stores 128 contiguous bytes per column)
 //   warp 4       allocates tensor memory; one thread of the leader CTA issues
 //                the tcgen05.mma of each K-half (3 products x Ms/16) and commits
 //                to the slot's `empty` mbarrier (and the accumulator's `accf`)
-//   warps 5-16   producers, one pass per tile each: read the unary and the four
+//   warps 5-19   producers: read the unary and the four
 //                incoming messages of their node(s) once, form the four
 //                exclusion products in the reference order, split hi / lo
 //                straight into the swizzled operand rows of the two K-half
 //                slots, and compute the normaliser s = sum_{x_j} colsum_f(x_j)
 //                h(x_j) (equal to the sum of the outputs up to rounding; the
-//                reference divides by that sum).  The next tile's inputs are
-//                loaded as soon as the products are formed, and prefetched into
-//                L2 two tiles ahead.
+//                reference divides by that sum).  Work items (tile, node slot)
+//                are claimed from a shared-memory counter, so the twelve warps
+//                run out of step and hide each other's load latency.
 // mbarriers: full[slot] (producers -> MMA), empty[slot] (MMA commit -> producers),
 // accf[stage] (MMA commit -> epilogue), accfree[stage] (epilogue -> MMA),
 // invf[tile % 4] (producers -> epilogue: the 1/s values).
@@ -54,12 +54,30 @@
 namespace sbp {
 namespace tc {
 
+#ifdef SBP_TC_TRACE
+// Debug build: cluster 0 records clock64 at the pipeline events of its first
+// TRACE_TILES tiles (tools/tc_trace.py prints the timeline).
+constexpr int TRACE_TILES = 48, TRACE_EVENTS = 16;
+__device__ long long g_tc_trace[TRACE_TILES * TRACE_EVENTS];
+#define TC_TRACE(tile_i, ev)                                                                    \
+    do {                                                                                        \
+        if (cluster == 0 && rank == 0 && lane == 0 && (tile_i) < TRACE_TILES)                   \
+            g_tc_trace[(tile_i) * TRACE_EVENTS + (ev)] = clock64();                             \
+    } while (0)
+#else
+#define TC_TRACE(tile_i, ev) do { } while (0)
+#endif
+
 constexpr int TC_NODES = 24;                // nodes per tile
 constexpr int TC_N = 4 * TC_NODES;          // MMA N = 96: (node, direction) columns per tile
 constexpr int TC_EPI_WARPS = 4;
-constexpr int TC_PROD_WARPS = 12;
+constexpr int TC_ITEMS = 12;                // producer work items per tile and CTA
+#ifndef SBP_TC_PROD_WARPS
+#define SBP_TC_PROD_WARPS 15                // 20 warps: the register cap (96) is that of 17
+#endif
+constexpr int TC_PROD_WARPS = SBP_TC_PROD_WARPS;
 constexpr int TC_WARPS = TC_EPI_WARPS + 1 + TC_PROD_WARPS;
-constexpr int TC_THREADS = 32 * TC_WARPS;   // 544
+constexpr int TC_THREADS = 32 * TC_WARPS;
 constexpr int TC_ACC = 2;                   // accumulator stages, 128 tensor-memory columns apart
 constexpr int TC_ACOL = 256;                // first tensor-memory column of the table operand(s)
 constexpr int TC_TCOLS = 512;
@@ -86,7 +104,7 @@ struct TcShape {
     static constexpr int AUX_BYTES = 3072;            // colsum, 1/s ring, mbarriers, tmem address
     static constexpr size_t SMEM = (size_t)A_BYTES + NSLOT * SLOT_BYTES + AUX_BYTES;
     static_assert(MS == 128 || MS == 256, "tensor-core dense kernel: Ms = 128 or 256");
-    static_assert(NPW * TC_PROD_WARPS == NCTA, "every producer warp forms its node(s) of every tile");
+    static_assert(NPW * TC_ITEMS == NCTA, "an item is one producer-warp pass: NPW nodes");
     static_assert(SLOT_BYTES == 49152 && SMEM <= 232448, "shared-memory budget");
 };
 
@@ -114,22 +132,32 @@ __device__ __forceinline__ void bar_arrive(unsigned long long *bar, unsigned ran
                          mapa(smem_u32(bar), rank)) : "memory");
 }
 
-// Bounded spin: a protocol error traps instead of hanging the device.  SLEEP
-// (ns) backs the producers' polling off so it does not take issue slots from
-// the warps that work.
+__device__ __forceinline__ void bar_arrive_relaxed(unsigned long long *bar, unsigned rank) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(smem_u32(bar), rank)) : "memory");
+}
+
+// Wait on an mbarrier phase.  try_wait suspends the thread in hardware for up
+// to the time hint, so waiting warps take no issue slots from working ones
+// (a polling loop did: 40 % of the executed instructions were polls).  Bounded:
+// a protocol error traps instead of hanging the device.
 template <int CG, int SLEEP>
 __device__ __forceinline__ void bar_wait(unsigned long long *bar, unsigned parity) {
     unsigned done = 0;
     for (unsigned spin = 0; !done; ++spin) {
         if (CG == 1)
-            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
-                         " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n"
+                         " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(20000u) : "memory");
         else
-            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-                         " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-        if (!done && SLEEP > 0) __nanosleep(SLEEP);
-        if (spin > (1u << 26)) __trap();
+            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
+                         " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity), "r"(20000u) : "memory");
+        if (spin > (1u << 24)) __trap();
     }
+}
+
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred;
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(pred));
+    return pred != 0;
 }
 
 __device__ __forceinline__ void st_global_if(float *p, float v, bool pred) {
@@ -140,10 +168,12 @@ __device__ __forceinline__ void st_global_if(float *p, float v, bool pred) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
+// Round to tf32 (10 explicit mantissa bits), nearest with ties away from zero,
+// on the bit pattern: add half a tf32 ulp and clear the 13 low bits.  Finite
+// non-negative inputs (tables and products of probabilities); cvt.rna.tf32.f32
+// compiles to a five-instruction sequence on sm_100a.
 __device__ __forceinline__ float tf32_rna(float x) {
-    unsigned u;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
-    return __uint_as_float(u);
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 descriptor
@@ -233,12 +263,15 @@ __device__ __forceinline__ void tmem_st32(unsigned taddr, const float (&v)[32]) 
         : "memory");
 }
 
-__device__ __forceinline__ void sts128(unsigned saddr, float a, float b, float c, float d) {
-    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+// (o0, o1) += (a0 * b0, a1 * b1)
+__device__ __forceinline__ void fma2v(float &o0, float &o1, float a0, float a1, float b0, float b1) {
+    unsigned long long r = f2_pack(o0, o1);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(r) : "l"(f2_pack(a0, a1)), "l"(f2_pack(b0, b1)));
+    f2_unpack(r, o0, o1);
 }
 
-__device__ __forceinline__ void l2_prefetch(const void *p, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ void sts128(unsigned saddr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(saddr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
 // ---- the kernel --------------------------------------------------------------
@@ -256,6 +289,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     unsigned long long *full = bars, *empty = bars + 4, *accf = bars + 8, *accfree = bars + 10,
                        *invf = bars + 12;
     unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 16);
+    unsigned *item_ctr = tmem_slot + 1;                // producers' work-item counter
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned rank = CG == 2 ? cluster_rank() : 0u;
@@ -293,14 +327,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     }
     if (tid == 0) {
         for (int s = 0; s < S::NSLOT; ++s) {
-            mbar_init(&full[s], TC_PROD_WARPS * CG);
+            mbar_init(&full[s], TC_ITEMS * CG);
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < TC_ACC; ++s) {
             mbar_init(&accf[s], 1);
             mbar_init(&accfree[s], TC_EPI_WARPS * CG);
         }
-        for (int s = 0; s < TC_INV; ++s) mbar_init(&invf[s], TC_PROD_WARPS * CG);
+        for (int s = 0; s < TC_INV; ++s) mbar_init(&invf[s], TC_ITEMS * CG);
+        *item_ctr = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == TC_EPI_WARPS) {
@@ -363,10 +398,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             bar_wait<CG, 0>(&invf[ir], (unsigned)((i / TC_INV) & 1));
             bar_wait<CG, 0>(&accf[acc], (unsigned)((i / TC_ACC) & 1));
             tc_fence_after();
+            if (warp == 0) TC_TRACE(i, 0);
             const float4 *iv4 = reinterpret_cast<const float4 *>(inv + ir * TC_N);
             const long long p0 = tile * TC_NODES;
-            int lr = a.lr_begin + (int)(p0 / W);
-            int c = (int)(p0 % W);
+            const unsigned lq = (unsigned)p0 / (unsigned)a.W;
+            int lr = a.lr_begin + (int)lq;
+            int c = (int)((unsigned)p0 - lq * (unsigned)a.W);
             long long off = ((long long)lr * W + c) * a.Ms;   // node's element offset in a slot plane
             long long left = npix - p0;                        // nodes of the strip from p0 on
 #pragma unroll 1
@@ -392,49 +429,57 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) bar_arrive<CG>(&accfree[acc], 0u);   // the leader's MMA thread waits on it
+            if (warp == 0) TC_TRACE(i, 1);
         }
     } else if (warp == TC_EPI_WARPS) {
         // ================= MMA issuer (leader CTA) =================
+        // The whole warp runs this code with warp-uniform values (descriptors
+        // stay in the uniform datapath); one elected lane issues.
         if (rank == 0) {
             const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_N >> 3) << 17) |
                                    ((unsigned)((128 * CG) >> 4) << 24);
-            const unsigned sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+            const unsigned long long a_desc0 = sw128_desc(smem_u32(sA));
+            const unsigned sB_u = smem_u32(sB);
             long long i = 0;
             for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
                 const int acc = (int)(i % TC_ACC);
                 bar_wait<CG, 0>(&accfree[acc], (unsigned)(((i / TC_ACC) & 1) ^ 1));
+                TC_TRACE(i, 2);
                 const unsigned d = tmem + 128 * acc;
-#pragma unroll 1
+#pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     const long long q = 2 * i + hh;
                     const int slot = (int)(q % S::NSLOT);
                     bar_wait<CG, 0>(&full[slot], (unsigned)((q / S::NSLOT) & 1));
                     tc_fence_after();
-                    if (lane == 0) {
-                        const unsigned bhi = sB_u + slot * S::SLOT_BYTES, blo = bhi + S::B_PLANE;
-                        // f_hi h_lo, f_lo h_hi (small terms first), then f_hi h_hi
-#pragma unroll 4
+                    TC_TRACE(i, 3 + 2 * hh);
+                    const unsigned long long bhi = sw128_desc(sB_u + slot * S::SLOT_BYTES);
+                    const unsigned long long blo = bhi + (S::B_PLANE >> 4);
+                    if (elect_one()) {
+                        // f_hi h_lo, f_lo h_hi (small terms first), then f_hi h_hi;
+                        // descriptor offsets are compile-time constants (>> 4: 16-byte units)
+#pragma unroll
                         for (int k = 0; k < S::KSTEPS; ++k) {
                             const int kk = hh * S::KSTEPS + k;
-                            const unsigned long long bd = sw128_desc(blo + (k >> 2) * S::B_ATOM + (k & 3) * 32);
+                            const unsigned long long bd = blo + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4);
                             if (S::A_HI_SMEM)
-                                mma_ss<CG>(d, sw128_desc(sA_u + (kk >> 2) * S::A_ATOM + (kk & 3) * 32), bd, idesc,
+                                mma_ss<CG>(d, a_desc0 + (((kk >> 2) * S::A_ATOM + (kk & 3) * 32) >> 4), bd, idesc,
                                            (hh | k) > 0);
                             else
                                 mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, (hh | k) > 0);
                         }
-#pragma unroll 4
+#pragma unroll
                         for (int k = 0; k < S::KSTEPS; ++k) {
                             const int kk = hh * S::KSTEPS + k;
                             mma_ts<CG>(d, tmem + S::ACOL_LO + 8 * kk,
-                                       sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32), idesc, 1u);
+                                       bhi + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4), idesc, 1u);
                         }
-#pragma unroll 4
+#pragma unroll
                         for (int k = 0; k < S::KSTEPS; ++k) {
                             const int kk = hh * S::KSTEPS + k;
-                            const unsigned long long bd = sw128_desc(bhi + (k >> 2) * S::B_ATOM + (k & 3) * 32);
+                            const unsigned long long bd = bhi + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4);
                             if (S::A_HI_SMEM)
-                                mma_ss<CG>(d, sw128_desc(sA_u + (kk >> 2) * S::A_ATOM + (kk & 3) * 32), bd, idesc, 1u);
+                                mma_ss<CG>(d, a_desc0 + (((kk >> 2) * S::A_ATOM + (kk & 3) * 32) >> 4), bd, idesc, 1u);
                             else
                                 mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, 1u);
                         }
@@ -442,26 +487,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                         if (hh == 1) mma_commit<CG>(&accf[acc]);
                     }
                     __syncwarp();
+                    TC_TRACE(i, 4 + 2 * hh);
                 }
             }
         }
     } else {
         // ================= producers =================
         constexpr int LP = S::LP, NPW = S::NPW;
-        const int pw = warp - TC_EPI_WARPS - 1;
+        // Work items are claimed from a per-CTA counter: item = (tile sequence
+        // number i, node slot pw of the tile).  Identical warps run at different
+        // speeds (they share schedulers with the MMA and epilogue warps), and a
+        // static warp -> node map made every tile wait for the slowest one.
         const int j = lane % LP, q = lane / LP;
-        const int nl = pw * NPW + q;                       // node within this CTA's share of the tile
         const unsigned sB_u = smem_u32(sB);
         float g[8], m[4][8];
         long long p, node_l, r;
-        int c;
+        int c, nl;
         bool valid;
-        auto locate = [&](long long tile) {
+        auto claim = [&]() -> unsigned {
+            unsigned it = 0;
+            if (lane == 0) it = atomicAdd(item_ctr, 1u);
+            return __shfl_sync(SBP_FULL_MASK, it, 0);
+        };
+        auto locate = [&](long long tile, int pw) {
+            nl = pw * NPW + q;                             // node within this CTA's share of the tile
             p = tile * TC_NODES + (long long)rank * S::NCTA + nl;
             valid = p < npix;
             if (!valid) p = npix - 1;
-            const int lr = a.lr_begin + (int)(p / a.W);
-            c = (int)(p % a.W);
+            const unsigned lq = (unsigned)p / (unsigned)a.W;      // strips hold < 2^31 nodes (launcher)
+            const int lr = a.lr_begin + (int)lq;
+            c = (int)((unsigned)p - lq * (unsigned)a.W);
             r = (long long)a.r0 + lr - 1;
             node_l = (long long)lr * a.W + c;
         };
@@ -494,25 +549,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                 }
             }
         };
-        auto prefetch = [&](long long tile) {
-            // one warp of the CTA: the tile's five contiguous input spans into L2
-            if (pw != 0 || lane >= 5 || tile >= tiles || (lane < 4 && a.first)) return;
-            const long long q0 = tile * TC_NODES + (long long)rank * S::NCTA;
-            if (q0 >= npix) return;
-            const long long n = npix - q0 < S::NCTA ? npix - q0 : S::NCTA;
-            const float *src = lane == 4
-                ? a.values + ((long long)(a.lr_begin - 1) * a.W + q0) * a.Ms
-                : a.msgs_in + lane * a.slot_stride + ((long long)a.lr_begin * a.W + q0) * a.Ms;
-            l2_prefetch(src, (unsigned)(n * a.Ms * 4));
-        };
-        if (cluster < tiles) {
-            locate(cluster);
+        // No loads stay in flight across the publishing fences / release
+        // arrives (they would wait for them, and the compiler spilled the
+        // in-flight registers): a warp exposes its own load latency, and the
+        // twelve warps, out of step through the item counter, hide each other's.
+        while (true) {
+            const unsigned item = claim();
+            const long long i = item / TC_ITEMS;
+            const int pw = (int)(item % TC_ITEMS);
+            const long long tile = cluster + i * nclusters;
+            if (tile >= tiles) break;
+            locate(tile, pw);
             load();
-            prefetch(cluster + nclusters);
-        }
-        long long i = 0;
-        for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
-            prefetch(tile + 2 * nclusters);
+            if (pw == 0) TC_TRACE(i, 7);
+            const int nl_cur = nl;
+            unsigned row_off[4];                           // this lane's 16-byte chunk of its node's four rows
+#pragma unroll
+            for (int d = 0; d < 4; ++d) row_off[d] = (unsigned)sw128_chunk(nl_cur * 4 + d, j, S::B_ATOM);
             const long long r_cur = r;
             const int c_cur = c;
             const bool valid_cur = valid;
@@ -529,45 +582,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             vmul(ab, ab, m[1]);
             vmul(h[0], ab, m[3]);         // excl 2 -> dir 0
             vmul(h[2], ab, m[2]);         // excl 3 -> dir 2
-            // the inputs are dead: fetch the next tile's while this one is split and stored
-            if (tile + nclusters < tiles) {
-                locate(tile + nclusters);
-                load();
-            }
-            float sd[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            if (pw == 0) TC_TRACE(i, 8);
+            const long long i_cur = i;
+            const int pw_cur = pw;
+            float sd[4][2] = {{0.0f, 0.0f}, {0.0f, 0.0f}, {0.0f, 0.0f}, {0.0f, 0.0f}};
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const long long qq = 2 * i + hh;
+                const long long qq = 2 * i_cur + hh;
                 const int slot = (int)(qq % S::NSLOT);
                 bar_wait<CG, 64>(&empty[slot], (unsigned)(((qq / S::NSLOT) & 1) ^ 1));
+                if (pw_cur == 0) TC_TRACE(i_cur, 9 + 2 * hh);
                 const unsigned slot_u = sB_u + slot * S::SLOT_BYTES;
                 const float4 cs4 = *reinterpret_cast<const float4 *>(csum + hh * S::KH + 4 * j);
-                const float cs[4] = {cs4.x, cs4.y, cs4.z, cs4.w};
 #pragma unroll
                 for (int d = 0; d < 4; ++d) {
-                    const int row = nl * 4 + d;            // column of this CTA's share of the tile
+                    const float *hv = &h[d][4 * hh];
                     float hi[4], lo[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float hv = h[d][4 * hh + u];
-                        hi[u] = tf32_rna(hv);
-                        lo[u] = hv - hi[u];
-                        sd[d] = fmaf(cs[u], hv, sd[d]);
-                    }
-                    const unsigned o = slot_u + sw128_chunk(row, j, S::B_ATOM);
+                    for (int u = 0; u < 4; ++u) hi[u] = tf32_rna(hv[u]);
+                    sub2(lo[0], lo[1], hv[0], hv[1], hi[0], hi[1]);
+                    sub2(lo[2], lo[3], hv[2], hv[3], hi[2], hi[3]);
+                    // normaliser partial sums (two lanes of a packed accumulator per direction)
+                    fma2v(sd[d][0], sd[d][1], cs4.x, cs4.y, hv[0], hv[1]);
+                    fma2v(sd[d][0], sd[d][1], cs4.z, cs4.w, hv[2], hv[3]);
+                    const unsigned o = slot_u + row_off[d];
                     sts128(o, hi[0], hi[1], hi[2], hi[3]);
                     sts128(o + S::B_PLANE, lo[0], lo[1], lo[2], lo[3]);
                 }
                 if (hh == 1) {
                     // 1/s of the node's four messages, before the slot is published
-                    const int ir = (int)(i % TC_INV);
+                    const int ir = (int)(i_cur % TC_INV);
                     float *iv = inv + ir * TC_N;
 #pragma unroll
                     for (int d = 0; d < 4; ++d) {
-                        const float s = lanes_sum<LP>(sd[d]);
+                        const float s = lanes_sum<LP>(sd[d][0] + sd[d][1]);
                         if (j == 0) {
                             const float rs = __frcp_rn(s);
-                            const int col = ((int)rank * S::NCTA + nl) * 4 + d;
+                            const int col = ((int)rank * S::NCTA + nl_cur) * 4 + d;
                             iv[col] = rs;
                             if (CG == 2)
                                 asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
@@ -582,13 +633,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
-                    bar_arrive<CG>(&full[slot], 0u);
-                    if (hh == 1) {
-                        const int ir = (int)(i % TC_INV);
-                        bar_arrive<CG>(&invf[ir], rank);
-                        if (CG == 2) bar_arrive<CG>(&invf[ir], rank ^ 1u);
+                    if (CG == 1) {
+                        bar_arrive<CG>(&full[slot], 0u);
+                        if (hh == 1) bar_arrive<CG>(&invf[(int)(i_cur % TC_INV)], rank);
+                    } else {
+                        // one cluster-scope release fence, then relaxed arrives (a
+                        // release arrive costs a membar each: 4 per tile and warp before)
+                        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                        bar_arrive_relaxed(&full[slot], 0u);
+                        if (hh == 1) {
+                            const int ir = (int)(i_cur % TC_INV);
+                            bar_arrive_relaxed(&invf[ir], rank);
+                            bar_arrive_relaxed(&invf[ir], rank ^ 1u);
+                        }
                     }
                 }
+                if (pw_cur == 0) TC_TRACE(i_cur, 10 + 2 * hh);
             }
         }
     }
@@ -641,6 +701,7 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
         }
     }
     const long long npix = (long long)(a.lr_end - a.lr_begin) * a.W;
+    if (npix >= (1ll << 31)) return cudaErrorNotSupported;   // 32-bit node coordinates in the kernel
     long long clusters = (npix + TC_NODES - 1) / TC_NODES;
     if (clusters <= 0) return cudaSuccess;
     if (clusters > clusters_max) clusters = clusters_max;
@@ -652,6 +713,17 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
 }  // namespace tc
 
 bool dense_tc_supported(int Ms) { return Ms == 128 || Ms == 256; }
+
+#ifdef SBP_TC_TRACE
+}  // namespace sbp
+extern "C" __attribute__((visibility("default"))) int sbp_debug_tc_trace(long long *out, int n) {
+    const int total = sbp::tc::TRACE_TILES * sbp::tc::TRACE_EVENTS;
+    if (n > total) n = total;
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpyFromSymbol(out, sbp::tc::g_tc_trace, sizeof(long long) * n);
+}
+namespace sbp {
+#endif
 
 cudaError_t launch_dense_tc(const DenseArgs &a, cudaStream_t s) {
     switch (a.Ms) {
