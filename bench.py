@@ -58,6 +58,15 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def tensor_tf32_peak():
+    """Dense tf32 tensor-core peak in TFLOP/s: half the measured bf16 rate
+    (MEASURED_PEAKS.json bf16_tflops, burst), else half the nominal 2250."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text()).get("bf16_tflops", 2250.0)) / 2
+    return 1125.0
+
+
 def algorithmic(cfg, pot):
     """Bytes / FLOPs per synchronous iteration: read every unary
     and every directed message once, write every directed message once;
@@ -457,7 +466,7 @@ def configs_block(args, torch, dev):
     launching stream, steady state), directed updates/s, the roofline
     max(B / HBM peak, F / FP32 peak) it is measured against, and the clocks
     sampled while it ran."""
-    from paper_1010_0012_b200 import synth
+    from paper_1010_0012_b200 import _lib, synth
     from paper_1010_0012_b200.engine import GridEngine
     hbm, _ = peaks()
     fp = fp32_peak()
@@ -492,6 +501,16 @@ def configs_block(args, torch, dev):
         bound = "hbm" if t_hbm >= t_fp else "fp32"
         roof = {"bound": bound, "ms": max(t_hbm, t_fp), "frac": max(t_hbm, t_fp) / ms,
                 "hbm_frac": t_hbm / ms, "fp32_frac": t_fp / ms}
+        if "dense_tc_kernel" in eng.kernel_name:
+            # 3xTF32 on the tensor cores: three tf32 MMA passes over the padded
+            # table; tf32 dense peak = half the measured bf16 rate
+            tf32 = tensor_tf32_peak()
+            Ms = eng.grid.Ms
+            t_tc = 3 * cfg.n_directed * 2 * Ms * Ms / (tf32 * 1e12) * 1e3
+            bound = "hbm" if t_hbm >= t_tc else "tensor"
+            roof = {"bound": bound, "ms": max(t_hbm, t_tc), "frac": max(t_hbm, t_tc) / ms,
+                    "hbm_frac": t_hbm / ms, "tensor_frac": t_tc / ms, "tf32_peak_tflops": tf32,
+                    "mma_passes": 3}
         if domain == "max" and kernel == "fast":
             # the max-sum band issues one FADD2 half + one FMNMX3 half per
             # candidate; its own instruction stream peaks below FFMA
@@ -514,15 +533,32 @@ def configs_block(args, torch, dev):
         for T in (2, 5, 9, 17, 33):
             cfg = synth.CONFIGS[f"C5_T{T}"]
             band = None
-            for kernel in ("fast", "standard"):
-                eng = GridEngine(synth.StripModel(cfg), domain, kernel, device=dev, values=vals)
-                e = measure(eng, cfg.iters if kernel == "fast" else 6, cfg, domain, kernel)
+            # dense arms: the default (sum-product: 3xTF32 on the tensor cores,
+            # max-sum: tiled SIMT) and, for sum-product, the SIMT kernel too
+            arms = [("fast", None), ("standard", None)]
+            if domain == "sum":
+                arms.append(("standard", "0"))
+            for kernel, tc in arms:
+                if tc is not None:
+                    os.environ["SBP_DENSE_TC"] = tc
+                    _lib.lib().sbp_reload_config()
+                try:
+                    eng = GridEngine(synth.StripModel(cfg), domain, kernel, device=dev, values=vals)
+                    e = measure(eng, cfg.iters if kernel == "fast" else 6, cfg, domain, kernel)
+                finally:
+                    if tc is not None:
+                        del os.environ["SBP_DENSE_TC"]
+                        _lib.lib().sbp_reload_config()
                 if kernel == "fast":
                     band = e
                 else:
-                    band["dense"] = {k: e[k] for k in ("kernel_name", "ms_per_iteration",
-                                                       "updates_per_s", "roofline")}
-                    band["speedup_band_over_dense"] = e["ms_per_iteration"] / band["ms_per_iteration"]
+                    key = "dense" if tc is None else "dense_simt"
+                    band[key] = {k: e[k] for k in ("kernel_name", "ms_per_iteration",
+                                                   "updates_per_s", "roofline")}
+                    if tc is None:
+                        band["speedup_band_over_dense"] = e["ms_per_iteration"] / band["ms_per_iteration"]
+                    else:
+                        band["speedup_band_over_dense_simt"] = e["ms_per_iteration"] / band["ms_per_iteration"]
                 del eng
                 torch.cuda.empty_cache()
             out["entries"].append(band)

@@ -51,6 +51,9 @@ FAMILIES = [
     ("chain", "C4", "sum", SEQUENTIAL, {}, "fast", None),
     ("chain_max", "C2", "max", SEQUENTIAL, {}, "fast", None),
     ("dense", "C3", "sum", SYNCHRONOUS, {}, "standard", None),
+    ("dense_simt_m128", "C4", "sum", SYNCHRONOUS, {"SBP_DENSE_TC": "0"}, "standard", None),
+    ("dense_tc", "C4", "sum", SYNCHRONOUS, {}, "standard", None),          # tcgen05, one CTA
+    ("dense_tc_pair", "C5_T9", "sum", SYNCHRONOUS, {}, "standard", None),  # tcgen05, CTA pair
     ("ell", "C2", "sum", SYNCHRONOUS, {}, "fast", "ell"),
     ("ell_f64", "C2", "sum", SYNCHRONOUS, {"SBP_PRECISION": "f64"}, "fast", "ell"),
     ("ell_chain", "C2", "max", SEQUENTIAL, {}, "fast", "ell"),

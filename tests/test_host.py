@@ -314,3 +314,33 @@ def test_band_without_compiled_radius_plans_as_ell(M, T):
     # a compiled radius still plans as a band
     assert plan.plan_potential(truncated_linear_potential(M, 0.5, 3.0), "sum", "fast", M,
                                Ms).kind == L.SBP_POT_BAND
+
+
+def _dense_name(Ms, domain, same_pointer, env=None, monkeypatch=None):
+    for k, v in (env or {}).items():
+        monkeypatch.setenv(k, v)
+    L.lib().sbp_reload_config()
+    s = L.SbpPotential()
+    s.kind = L.SBP_POT_DENSE
+    s.domain = L.SBP_SUM if domain == "sum" else L.SBP_MAX
+    s.dense_t[0] = 0x1000                      # never dereferenced by sbp_plan_name
+    s.dense_t[1] = 0x1000 if same_pointer else 0x2000
+    g = L.SbpGrid(64, 64, Ms, Ms, 0, 64, L.SBP_DEVICE_AUTO)
+    buf = ctypes.create_string_buffer(128)
+    L.check(L.lib().sbp_plan_name(ctypes.byref(g), ctypes.byref(s), 0, buf, 128))
+    return buf.value.decode()
+
+
+def test_dense_kernel_choice(monkeypatch):
+    """Sum-product with ONE table pointer for both orientations (a symmetric
+    table) runs on the tensor cores at Ms = 128 / 256; everything else keeps
+    the tiled SIMT kernel (include/sbp.h, sbp_potential.dense_t)."""
+    assert _dense_name(128, "sum", True) == "dense_tc_kernel<sum,Ms=128,3xTF32>"
+    assert _dense_name(256, "sum", True) == "dense_tc_kernel<sum,Ms=256,3xTF32>"
+    assert _dense_name(256, "sum", False) == "dense_iter_kernel<sum,Ms=256>"
+    assert _dense_name(64, "sum", True) == "dense_iter_kernel<sum,Ms=64>"
+    assert _dense_name(256, "max", True) == "dense_iter_kernel<max,Ms=256>"
+    assert _dense_name(128, "sum", True, {"SBP_DENSE_TC": "0"}, monkeypatch) == \
+        "dense_iter_kernel<sum,Ms=128>"
+    monkeypatch.undo()
+    L.lib().sbp_reload_config()
