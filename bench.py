@@ -412,7 +412,7 @@ def run_ours(args, cfg):
     cpu = None
     others = None
     if world == 1 and not args.kernel_only and not args.no_configs:
-        others = configs_block(args, torch, dev)
+        others = configs_block_isolated()
     if not args.kernel_only:
         if world == 1:
             e2e = e2e_public_api(args, cfg, torch)
@@ -566,6 +566,22 @@ def configs_block(args, torch, dev):
     return out
 
 
+def configs_block_isolated():
+    """configs_block in a child process (`bench.py --configs-only`): its
+    kernels (tensor cores, CTA pairs, every band width) get their own CUDA
+    context, so a failure there is reported in the line instead of taking the
+    headline measurement down with it."""
+    try:
+        r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--configs-only"],
+                           capture_output=True, text=True, timeout=1200)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if r.returncode == 0 and lines:
+            return json.loads(lines[-1])
+        return {"error": f"configs child rc={r.returncode}: {r.stderr.strip()[-300:]}"}
+    except Exception as e:   # timeout, spawn failure
+        return {"error": f"configs child: {type(e).__name__}: {e}"}
+
+
 def e2e_public_api(args, cfg, torch):
     """End to end through the public API with host buffers, two ways:
 
@@ -702,7 +718,14 @@ def main():
                     help="skip the e2e, CPU-baseline and other-config legs (kernel A/B runs)")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the other-config block (C3, C5 band-width sweep)")
+    ap.add_argument("--configs-only", action="store_true",
+                    help="print the other-config block (C3, C5 sweep) as one JSON line and exit")
     args = ap.parse_args()
+    if args.configs_only:
+        import torch
+        torch.cuda.set_device(0)
+        print(json.dumps(configs_block(args, torch, torch.device("cuda", 0))))
+        return
     from paper_1010_0012_b200 import synth
     cfg = synth.CONFIGS[args.config]
     args.domain = args.domain or cfg.domains[0]
