@@ -36,7 +36,7 @@
 //   warp 4       allocates tensor memory; one thread of the leader CTA issues
 //                the tcgen05.mma of each K-half (3 products x Ms/16) and commits
 //                to the slot's `empty` mbarrier (and the accumulator's `accf`)
-//   warps 5-19   producers: read the unary and the four
+//   warps 5-19   producers (5-18 in a CTA pair): read the unary and the four
 //                incoming messages of their node(s) once, form the four
 //                exclusion products in the reference order, split hi / lo
 //                straight into the swizzled operand rows of the two K-half
@@ -45,9 +45,14 @@
 //                reference divides by that sum).  Work items (tile, node slot)
 //                are claimed from a shared-memory counter, so the twelve warps
 //                run out of step and hide each other's load latency.
+//   warp 19     (CTA pairs) relay: forwards the peer CTA's `full` arrivals to the
+//                leader and copies this CTA's 1/s values to the other CTA, one
+//                cluster-scope release fence per event instead of one per
+//                producer warp and K-half
 // mbarriers: full[slot] (producers -> MMA), empty[slot] (MMA commit -> producers),
 // accf[stage] (MMA commit -> epilogue), accfree[stage] (epilogue -> MMA),
-// invf[tile % 4] (producers -> epilogue: the 1/s values).
+// linv[tile % 4] (producers -> epilogue / relay: the CTA's 1/s values),
+// invf[tile % 4] (relay -> the other CTA's epilogue).
 #include "aux_kernels.cuh"
 #include "band_kernel.cuh"   // vmul, lanes_sum, smem_u32, mbar_init
 
@@ -101,6 +106,8 @@ struct TcShape {
     static constexpr int A_BYTES = A_HI_SMEM ? (MS / 32) * A_ATOM : 0;
     static constexpr int ACOL_HI = TC_ACOL;           // Ms = 128 only
     static constexpr int ACOL_LO = MS == 128 ? TC_ACOL + 128 : TC_ACOL;
+    static constexpr int RELAY = CG == 2 ? 1 : 0;     // pairs: the last warp relays, 14 produce
+    static constexpr int THREADS = TC_THREADS;        // 640: more threads would cap registers at 80
     static constexpr int AUX_BYTES = 3072;            // colsum, 1/s ring, mbarriers, tmem address
     static constexpr size_t SMEM = (size_t)A_BYTES + NSLOT * SLOT_BYTES + AUX_BYTES;
     static_assert(MS == 128 || MS == 256, "tensor-core dense kernel: Ms = 128 or 256");
@@ -277,7 +284,7 @@ __device__ __forceinline__ void sts128(unsigned saddr, float a, float b, float c
 // ---- the kernel --------------------------------------------------------------
 
 template <int MS>
-__global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_constant__ DenseArgs a) {
+__global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const __grid_constant__ DenseArgs a) {
     using S = TcShape<MS>;
     constexpr int CG = S::CG;
     extern __shared__ __align__(1024) unsigned char tc_smem[];
@@ -287,8 +294,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     float *inv = csum + MS;                                                   // [TC_INV][TC_N]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(inv + TC_INV * TC_N);
     unsigned long long *full = bars, *empty = bars + 4, *accf = bars + 8, *accfree = bars + 10,
-                       *invf = bars + 12;
-    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 16);
+                       *invf = bars + 12, *linv = bars + 16;
+    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 20);
     unsigned *item_ctr = tmem_slot + 1;                // producers' work-item counter
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
 
     // ---- one-time setup: table operands, column sums, barriers, tensor memory
     if (S::A_HI_SMEM) {
-        for (int i = tid; i < 128 * (MS / 4); i += TC_THREADS) {
+        for (int i = tid; i < 128 * (MS / 4); i += S::THREADS) {
             const int row = i / (MS / 4), ch = i % (MS / 4);
             const float4 v = *reinterpret_cast<const float4 *>(tab + (size_t)(128 * rank + row) * MS + 4 * ch);
             sts128(smem_u32(sA) + sw128_chunk(row, ch, S::A_ATOM), tf32_rna(v.x), tf32_rna(v.y),
@@ -327,14 +334,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
     }
     if (tid == 0) {
         for (int s = 0; s < S::NSLOT; ++s) {
-            mbar_init(&full[s], TC_ITEMS * CG);
+            // the leader's `full` counts its own producers' items and, in a
+            // pair, one forwarded arrival from the peer's relay warp
+            mbar_init(&full[s], TC_ITEMS + (CG == 2 && rank == 0 ? 1 : 0));
             mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < TC_ACC; ++s) {
             mbar_init(&accf[s], 1);
             mbar_init(&accfree[s], TC_EPI_WARPS * CG);
         }
-        for (int s = 0; s < TC_INV; ++s) mbar_init(&invf[s], TC_ITEMS * CG);
+        for (int s = 0; s < TC_INV; ++s) {
+            mbar_init(&linv[s], TC_ITEMS);   // this CTA's producers: their 1/s values are written
+            mbar_init(&invf[s], 1);          // pair: the peer's relay has copied its half over
+        }
         *item_ctr = 0u;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -395,7 +407,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
         long long i = 0;
         for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
             const int acc = (int)(i % TC_ACC), ir = (int)(i % TC_INV);
-            bar_wait<CG, 0>(&invf[ir], (unsigned)((i / TC_INV) & 1));
+            bar_wait<1, 0>(&linv[ir], (unsigned)((i / TC_INV) & 1));
+            if (CG == 2) bar_wait<CG, 0>(&invf[ir], (unsigned)((i / TC_INV) & 1));
             bar_wait<CG, 0>(&accf[acc], (unsigned)((i / TC_ACC) & 1));
             tc_fence_after();
             if (warp == 0) TC_TRACE(i, 0);
@@ -428,7 +441,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive<CG>(&accfree[acc], 0u);   // the leader's MMA thread waits on it
+            if (lane == 0) {                                    // the leader's MMA thread waits on it
+                if (rank == 0) bar_arrive<1>(&accfree[acc], 0u);
+                else bar_arrive<CG>(&accfree[acc], 0u);
+            }
             if (warp == 0) TC_TRACE(i, 1);
         }
     } else if (warp == TC_EPI_WARPS) {
@@ -490,6 +506,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                     TC_TRACE(i, 4 + 2 * hh);
                 }
             }
+        }
+    } else if (S::RELAY && warp == TC_WARPS - 1) {
+        // ================= relay (CTA pairs) =================
+        // Forwards this CTA's producer progress to the peer with ONE
+        // cluster-scope release per event: the peer CTA's `full` arrivals to
+        // the leader's barrier, and this CTA's half of the 1/s vector to the
+        // other CTA's epilogue.
+        long long i = 0;
+        for (long long tile = cluster; tile < tiles; tile += nclusters, ++i) {
+            const int ir = (int)(i % TC_INV);
+            if (rank == 1) {
+                const long long q0 = 2 * i;
+                const int s0 = (int)(q0 % S::NSLOT);
+                bar_wait<1, 0>(&full[s0], (unsigned)((q0 / S::NSLOT) & 1));
+                if (lane == 0) {
+                    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                    bar_arrive_relaxed(&full[s0], 0u);
+                }
+                const long long q1 = q0 + 1;
+                const int s1 = (int)(q1 % S::NSLOT);
+                bar_wait<1, 0>(&full[s1], (unsigned)((q1 / S::NSLOT) & 1));
+            }
+            bar_wait<1, 0>(&linv[ir], (unsigned)((i / TC_INV) & 1));
+            float *mine = inv + ir * TC_N + (int)rank * S::NB;
+            for (int c = lane; c < S::NB; c += 32)
+                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(mapa(smem_u32(mine + c), rank ^ 1u)),
+                             "f"(mine[c]) : "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                if (rank == 1) bar_arrive_relaxed(&full[(int)((2 * i + 1) % S::NSLOT)], 0u);
+                bar_arrive_relaxed(&invf[ir], rank ^ 1u);
+            }
+            __syncwarp();
         }
     } else {
         // ================= producers =================
@@ -619,10 +669,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                         if (j == 0) {
                             const float rs = __frcp_rn(s);
                             const int col = ((int)rank * S::NCTA + nl_cur) * 4 + d;
-                            iv[col] = rs;
-                            if (CG == 2)
-                                asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(
-                                                 mapa(smem_u32(iv + col), rank ^ 1u)), "f"(rs) : "memory");
+                            iv[col] = rs;               // a pair's relay warp copies it to the peer
                             const bool ok = (s > 0.0f) && !isinf(s);
                             if (!ok && valid_cur && has[d])
                                 report_failure(a.err, a.iteration, directed_edge_id(a.H, a.W, r_cur, c_cur, d));
@@ -633,20 +680,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) dense_tc_kernel(const __grid_co
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) {
-                    if (CG == 1) {
-                        bar_arrive<CG>(&full[slot], 0u);
-                        if (hh == 1) bar_arrive<CG>(&invf[(int)(i_cur % TC_INV)], rank);
-                    } else {
-                        // one cluster-scope release fence, then relaxed arrives (a
-                        // release arrive costs a membar each: 4 per tile and warp before)
-                        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-                        bar_arrive_relaxed(&full[slot], 0u);
-                        if (hh == 1) {
-                            const int ir = (int)(i_cur % TC_INV);
-                            bar_arrive_relaxed(&invf[ir], rank);
-                            bar_arrive_relaxed(&invf[ir], rank ^ 1u);
-                        }
-                    }
+                    // CTA-scope releases only: in a pair the relay warp forwards
+                    // (a cluster-scope fence here cost ~1500 cycles per half and warp)
+                    bar_arrive<1>(&full[slot], 0u);
+                    if (hh == 1) bar_arrive<1>(&linv[(int)(i_cur % TC_INV)], 0u);
                 }
                 if (pw_cur == 0) TC_TRACE(i_cur, 10 + 2 * hh);
             }
@@ -680,7 +717,7 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cfg.blockDim = dim3(TC_THREADS);
+    cfg.blockDim = dim3(S::THREADS);
     cfg.dynamicSmemBytes = S::SMEM;
     cfg.stream = s;
     if (!clusters_max) {
