@@ -53,7 +53,7 @@ cudaError_t launch_dense(int domain, const DenseArgs &a, cudaStream_t s);
 // Sum-product, symmetric table (t[0] serves both orientations), Ms = 128 or
 // 256: the same update as a 3xTF32 GEMM on the tensor cores (dense_tc_kernel.cu).
 bool dense_tc_supported(int Ms);
-cudaError_t launch_dense_tc(const DenseArgs &a, cudaStream_t s);
+cudaError_t launch_dense_tc(const DenseArgs &a, bool bf16_corrections, cudaStream_t s);
 
 
 

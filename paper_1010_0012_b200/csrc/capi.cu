@@ -114,7 +114,8 @@ struct EnvKnobs {
     int tap_staged = env_int_raw("SBP_TAP_STAGED", -1);
     int tap_rolled = env_int_raw("SBP_TAP_ROLLED", -1);
     int max_blocks = env_int_raw("SBP_MAX_BLOCKS", 0);
-    int dense_tc = env_int_raw("SBP_DENSE_TC", 1);   // dense sum-product on the tensor cores (0: SIMT)
+    int dense_tc = env_int_raw("SBP_DENSE_TC", 1);   // dense sum-product on the tensor cores: 1 3xTF32,
+                                                      // 2 bf16 correction products (faster, 5.7e-6), 0 SIMT
     int tap_lift = env_int_raw("SBP_TAP_LIFT", 1);   // sum, Ms >= 128: R = 5..7 bands run on the R = 8 tap kernel
 };
 EnvKnobs &knobs() {
@@ -503,7 +504,7 @@ static int iterate_impl(const sbp_grid *g, const sbp_potential *pot, const float
         a.t[0] = pot->dense_t[0];
         a.t[1] = pot->dense_t[1];
         if (dense_on_tensor_cores(g, pot))
-            return cuda_status(sbp::launch_dense_tc(a, s), "sbp_iterate(dense, tensor cores)");
+            return cuda_status(sbp::launch_dense_tc(a, knobs().dense_tc == 2, s), "sbp_iterate(dense, tensor cores)");
         return cuda_status(sbp::launch_dense(pot->domain, a, s), "sbp_iterate(dense)");
     }
     if (pot->kind == SBP_POT_ELL || pot->kind == SBP_POT_DENSE) {
@@ -674,7 +675,8 @@ int sbp_plan_name(const sbp_grid *g, const sbp_potential *pot, int sequential, c
         }
     } else if (pot->kind == SBP_POT_DENSE && g->Ms >= 32) {
         if (sequential == 0 && dense_on_tensor_cores(g, pot))
-            snprintf(buf, len, "dense_tc_kernel<sum,Ms=%d,3xTF32>", g->Ms);
+            snprintf(buf, len, "dense_tc_kernel<sum,Ms=%d,%s>", g->Ms,
+                     knobs().dense_tc == 2 ? "TF32+2xBF16" : "3xTF32");
         else
             snprintf(buf, len, "dense_iter_kernel<%s,Ms=%d>", dom, g->Ms);
     } else {

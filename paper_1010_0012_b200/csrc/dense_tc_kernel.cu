@@ -8,7 +8,11 @@
 // in 3xTF32: f = f_hi + f_lo, h = h_hi + h_lo (hi = the value rounded to
 // tf32, lo = the exact fp32 remainder), out = f_hi h_lo + f_lo h_hi + f_hi h_hi
 // accumulated in fp32 by the tensor core (the dropped f_lo h_lo term is
-// 2^-22 relative).  Symmetric tables only (one resident copy serves both
+// 2^-22 relative).  Variant C16 (SBP_DENSE_TC=2, opt-in) runs the two
+// correction products in bf16 (kind::f16, K = 16 per MMA instead of 8) into
+// the same accumulator: 64 instead of 96 MMAs per Ms = 256 tile, 2.47 vs
+// 2.63 ms per C5 iteration, but 5.7e-6 instead of 3.2e-6 from the f64 oracle --
+// too close to the 1e-5 bar to be the default.  Symmetric tables only (one resident copy serves both
 // orientations), Ms = 128 (one CTA) or Ms = 256 (a CTA pair, cta_group::2,
 // each CTA owning 128 of the 256 output labels).
 //
@@ -88,7 +92,7 @@ constexpr int TC_ACOL = 256;                // first tensor-memory column of the
 constexpr int TC_TCOLS = 512;
 constexpr int TC_INV = 4;                   // ring of per-tile 1/s vectors
 
-template <int MS>
+template <int MS, bool C16 = false>
 struct TcShape {
     static constexpr int CG = MS / 128;               // CTAs per MMA (cta_group)
     static constexpr int NB = TC_N / CG;              // tile columns (B rows) held by one CTA
@@ -96,16 +100,24 @@ struct TcShape {
     static constexpr int LP = MS / 8;                 // lanes per node (8 labels each)
     static constexpr int NPW = 32 / LP;               // nodes per producer warp
     static constexpr int KH = MS / 2;                 // labels per K-half
-    static constexpr int KSTEPS = KH / 8;             // MMAs (K = 8) per product and K-half
+    static constexpr int KSTEPS = KH / 8;             // tf32 MMAs (K = 8) per K-half: f_hi h_hi
+    static constexpr int KSTEPS16 = KH / 16;          // bf16 MMAs (K = 16) per K-half and correction
     static constexpr int B_ATOM = NB * 128;           // bytes: NB rows x 32 tf32
-    static constexpr int B_PLANE = (KH / 32) * B_ATOM;
-    static constexpr int SLOT_BYTES = 2 * B_PLANE;    // hi and lo planes: 48 KB
+    static constexpr int B_PLANE = (KH / 32) * B_ATOM;     // a tf32 plane (32 per 128-byte row): h_hi, h_lo
+    static constexpr int B_PLANE16 = (KH / 64) * B_ATOM;   // C16: bf16 planes (64 per row): bf16(h), bf16(h_lo)
+    static constexpr int SLOT_BYTES = 2 * B_PLANE;         // 48 KB either way (2 B_PLANE16 = B_PLANE)
     static constexpr int NSLOT = MS == 128 ? 4 : 2;
     static constexpr bool A_HI_SMEM = MS == 256;      // f_hi in shared memory (no room in tensor memory)
     static constexpr int A_ATOM = 128 * 128;          // bytes: 128 rows x 32 tf32
     static constexpr int A_BYTES = A_HI_SMEM ? (MS / 32) * A_ATOM : 0;
-    static constexpr int ACOL_HI = TC_ACOL;           // Ms = 128 only
+    // tensor-memory columns of the table operands: f_hi as tf32 (Ms = 128 only,
+    // one column per k), then f_lo as tf32 -- or, C16, bf16(f_lo) and bf16(f),
+    // two k per column
+    static constexpr int ACOL_HI = TC_ACOL;
     static constexpr int ACOL_LO = MS == 128 ? TC_ACOL + 128 : TC_ACOL;
+    static constexpr int ACOL_LO16 = ACOL_LO;
+    static constexpr int ACOL_HI16 = ACOL_LO16 + MS / 2;
+    static_assert(ACOL_LO + MS <= TC_TCOLS, "tensor-memory budget");
     static constexpr int RELAY = CG == 2 ? 1 : 0;     // pairs: the last warp relays, 14 produce
     static constexpr int THREADS = TC_THREADS;        // 640: more threads would cap registers at 80
     static constexpr int AUX_BYTES = 3072;            // colsum, 1/s ring, mbarriers, tmem address
@@ -223,6 +235,20 @@ __device__ __forceinline__ void mma_ts(unsigned d, unsigned a_tmem, unsigned lon
                      "l"(b), "r"(idesc), "r"(acc) : "memory");
 }
 
+// kind::f16 with bf16 operands (A: two k per tensor-memory column), same fp32 accumulator
+template <int CG>
+__device__ __forceinline__ void mma_ts16(unsigned d, unsigned a_tmem, unsigned long long b, unsigned idesc,
+                                         unsigned acc) {
+    if (CG == 1)
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a_tmem),
+                     "l"(b), "r"(idesc), "r"(acc) : "memory");
+    else
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a_tmem),
+                     "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+
 template <int CG>
 __device__ __forceinline__ void mma_commit(unsigned long long *bar) {
     if (CG == 1)
@@ -270,6 +296,17 @@ __device__ __forceinline__ void tmem_st32(unsigned taddr, const float (&v)[32]) 
         : "memory");
 }
 
+// two floats -> one 32-bit word of bf16 (a in the low half: the lower k / label)
+__device__ __forceinline__ float pack_bf16(float a, float b) {
+    unsigned r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void sts64(unsigned saddr, float a, float b) {
+    asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(saddr), "f"(a), "f"(b) : "memory");
+}
+
 // (o0, o1) += (a0 * b0, a1 * b1)
 __device__ __forceinline__ void fma2v(float &o0, float &o1, float a0, float a1, float b0, float b1) {
     unsigned long long r = f2_pack(o0, o1);
@@ -283,9 +320,10 @@ __device__ __forceinline__ void sts128(unsigned saddr, float a, float b, float c
 
 // ---- the kernel --------------------------------------------------------------
 
-template <int MS>
-__global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const __grid_constant__ DenseArgs a) {
-    using S = TcShape<MS>;
+template <int MS, bool C16>
+__global__ void __launch_bounds__(TcShape<MS, C16>::THREADS, 1)
+dense_tc_kernel(const __grid_constant__ DenseArgs a) {
+    using S = TcShape<MS, C16>;
     constexpr int CG = S::CG;
     extern __shared__ __align__(1024) unsigned char tc_smem[];
     unsigned char *sA = tc_smem;                       // Ms = 256: f_hi
@@ -293,9 +331,14 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
     float *csum = reinterpret_cast<float *>(sB + S::NSLOT * S::SLOT_BYTES);   // [MS]
     float *inv = csum + MS;                                                   // [TC_INV][TC_N]
     unsigned long long *bars = reinterpret_cast<unsigned long long *>(inv + TC_INV * TC_N);
-    unsigned long long *full = bars, *empty = bars + 4, *accf = bars + 8, *accfree = bars + 10,
-                       *invf = bars + 12, *linv = bars + 16;
-    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 20);
+    // `empty` has two generations per slot: a parity wait cannot tell phase k
+    // from phase k + 2, and a producer that claimed an item early can be two
+    // uses of a slot ahead of the MMA (it overwrote live operand rows once);
+    // with use u on barrier [slot + NSLOT (u % 2)] the alias is four uses away,
+    // further than the item counter lets any warp run ahead.
+    unsigned long long *full = bars, *empty = bars + 4, *accf = bars + 12, *accfree = bars + 14,
+                       *invf = bars + 16, *linv = bars + 20;
+    unsigned *tmem_slot = reinterpret_cast<unsigned *>(bars + 24);
     unsigned *item_ctr = tmem_slot + 1;                // producers' work-item counter
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -338,6 +381,7 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
             // pair, one forwarded arrival from the peer's relay warp
             mbar_init(&full[s], TC_ITEMS + (CG == 2 && rank == 0 ? 1 : 0));
             mbar_init(&empty[s], 1);
+            mbar_init(&empty[s + S::NSLOT], 1);
         }
         for (int s = 0; s < TC_ACC; ++s) {
             mbar_init(&accf[s], 1);
@@ -369,18 +413,39 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
         // table rows of this CTA -> tensor memory: lane = label row, column = k
         const float *row = tab + (size_t)(128 * rank + 32 * warp + lane) * MS;
         const unsigned lane_base = tmem + ((unsigned)(32 * warp) << 16);
-        for (int k0 = 0; k0 < MS; k0 += 32) {
-            float hi[32], lo[32];
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-                const float4 t = *reinterpret_cast<const float4 *>(row + k0 + i);
-                hi[i] = tf32_rna(t.x); hi[i + 1] = tf32_rna(t.y);
-                hi[i + 2] = tf32_rna(t.z); hi[i + 3] = tf32_rna(t.w);
-                lo[i] = t.x - hi[i]; lo[i + 1] = t.y - hi[i + 1];
-                lo[i + 2] = t.z - hi[i + 2]; lo[i + 3] = t.w - hi[i + 3];
+        if constexpr (C16) {
+            for (int k0 = 0; k0 < MS; k0 += 64) {
+                float lo16[32], hi16[32];   // packed bf16 pairs: columns (k0 / 2) .. + 31
+    #pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    float hi[32];
+    #pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const float2 t = *reinterpret_cast<const float2 *>(row + k0 + 32 * half + i);
+                        hi[i] = tf32_rna(t.x);
+                        hi[i + 1] = tf32_rna(t.y);
+                        lo16[16 * half + i / 2] = pack_bf16(t.x - hi[i], t.y - hi[i + 1]);
+                        hi16[16 * half + i / 2] = pack_bf16(t.x, t.y);
+                    }
+                    if (!S::A_HI_SMEM) tmem_st32(lane_base + S::ACOL_HI + k0 + 32 * half, hi);
+                }
+                tmem_st32(lane_base + S::ACOL_LO16 + k0 / 2, lo16);
+                tmem_st32(lane_base + S::ACOL_HI16 + k0 / 2, hi16);
             }
-            if (!S::A_HI_SMEM) tmem_st32(lane_base + S::ACOL_HI + k0, hi);
-            tmem_st32(lane_base + S::ACOL_LO + k0, lo);
+        } else {
+            for (int k0 = 0; k0 < MS; k0 += 32) {
+                float hi[32], lo[32];
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 t = *reinterpret_cast<const float4 *>(row + k0 + i);
+                    hi[i] = tf32_rna(t.x); hi[i + 1] = tf32_rna(t.y);
+                    hi[i + 2] = tf32_rna(t.z); hi[i + 3] = tf32_rna(t.w);
+                    lo[i] = t.x - hi[i]; lo[i + 1] = t.y - hi[i + 1];
+                    lo[i + 2] = t.z - hi[i + 2]; lo[i + 3] = t.w - hi[i + 3];
+                }
+                if (!S::A_HI_SMEM) tmem_st32(lane_base + S::ACOL_HI + k0, hi);
+                tmem_st32(lane_base + S::ACOL_LO + k0, lo);
+            }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -452,8 +517,9 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
         // The whole warp runs this code with warp-uniform values (descriptors
         // stay in the uniform datapath); one elected lane issues.
         if (rank == 0) {
-            const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)(TC_N >> 3) << 17) |
-                                   ((unsigned)((128 * CG) >> 4) << 24);
+            const unsigned mn = ((unsigned)(TC_N >> 3) << 17) | ((unsigned)((128 * CG) >> 4) << 24);
+            const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | mn;     // tf32 x tf32 -> f32
+            const unsigned idesc16 = (1u << 4) | (1u << 7) | (1u << 10) | mn;   // bf16 x bf16 -> f32
             const unsigned long long a_desc0 = sw128_desc(smem_u32(sA));
             const unsigned sB_u = smem_u32(sB);
             long long i = 0;
@@ -470,28 +536,47 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
                     tc_fence_after();
                     TC_TRACE(i, 3 + 2 * hh);
                     const unsigned long long bhi = sw128_desc(sB_u + slot * S::SLOT_BYTES);
-                    const unsigned long long blo = bhi + (S::B_PLANE >> 4);
+                    const unsigned long long blo = bhi + (S::B_PLANE >> 4);      // h_lo (tf32), or, C16:
+                    const unsigned long long bhi16 = blo;                          // bf16(h), then bf16(h_lo)
+                    const unsigned long long blo16 = bhi16 + (S::B_PLANE16 >> 4);
                     if (elect_one()) {
-                        // f_hi h_lo, f_lo h_hi (small terms first), then f_hi h_hi;
-                        // descriptor offsets are compile-time constants (>> 4: 16-byte units)
+                        // corrections first (small terms), then f_hi h_hi, all into one fp32
+                        // accumulator; descriptor offsets are compile-time constants (>> 4:
+                        // 16-byte units)
+                        if constexpr (C16) {
 #pragma unroll
-                        for (int k = 0; k < S::KSTEPS; ++k) {
-                            const int kk = hh * S::KSTEPS + k;
-                            const unsigned long long bd = blo + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4);
-                            if (S::A_HI_SMEM)
-                                mma_ss<CG>(d, a_desc0 + (((kk >> 2) * S::A_ATOM + (kk & 3) * 32) >> 4), bd, idesc,
-                                           (hh | k) > 0);
-                            else
-                                mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, (hh | k) > 0);
+                            for (int k = 0; k < S::KSTEPS16; ++k) {         // bf16(f_lo) bf16(h)
+                                const int kk = hh * S::KSTEPS16 + k;
+                                mma_ts16<CG>(d, tmem + S::ACOL_LO16 + 8 * kk,
+                                             bhi16 + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4), idesc16,
+                                             (hh | k) > 0);
+                            }
+#pragma unroll
+                            for (int k = 0; k < S::KSTEPS16; ++k) {         // bf16(f) bf16(h_lo)
+                                const int kk = hh * S::KSTEPS16 + k;
+                                mma_ts16<CG>(d, tmem + S::ACOL_HI16 + 8 * kk,
+                                             blo16 + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4), idesc16, 1u);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < S::KSTEPS; ++k) {           // f_hi h_lo
+                                const int kk = hh * S::KSTEPS + k;
+                                const unsigned long long bd = blo + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4);
+                                if (S::A_HI_SMEM)
+                                    mma_ss<CG>(d, a_desc0 + (((kk >> 2) * S::A_ATOM + (kk & 3) * 32) >> 4), bd,
+                                               idesc, (hh | k) > 0);
+                                else
+                                    mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, (hh | k) > 0);
+                            }
+#pragma unroll
+                            for (int k = 0; k < S::KSTEPS; ++k) {           // f_lo h_hi
+                                const int kk = hh * S::KSTEPS + k;
+                                mma_ts<CG>(d, tmem + S::ACOL_LO + 8 * kk,
+                                           bhi + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4), idesc, 1u);
+                            }
                         }
 #pragma unroll
-                        for (int k = 0; k < S::KSTEPS; ++k) {
-                            const int kk = hh * S::KSTEPS + k;
-                            mma_ts<CG>(d, tmem + S::ACOL_LO + 8 * kk,
-                                       bhi + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4), idesc, 1u);
-                        }
-#pragma unroll
-                        for (int k = 0; k < S::KSTEPS; ++k) {
+                        for (int k = 0; k < S::KSTEPS; ++k) {               // f_hi h_hi
                             const int kk = hh * S::KSTEPS + k;
                             const unsigned long long bd = bhi + (((k >> 2) * S::B_ATOM + (k & 3) * 32) >> 4);
                             if (S::A_HI_SMEM)
@@ -499,7 +584,8 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
                             else
                                 mma_ts<CG>(d, tmem + S::ACOL_HI + 8 * kk, bd, idesc, 1u);
                         }
-                        mma_commit<CG>(&empty[slot]);          // the slot is free once these complete
+                        // the slot is free once these complete: use u of the slot, generation u % 2
+                        mma_commit<CG>(&empty[slot + S::NSLOT * (int)((q / S::NSLOT) & 1)]);
                         if (hh == 1) mma_commit<CG>(&accf[acc]);
                     }
                     __syncwarp();
@@ -613,9 +699,13 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
             load();
             if (pw == 0) TC_TRACE(i, 7);
             const int nl_cur = nl;
-            unsigned row_off[4];                           // this lane's 16-byte chunk of its node's four rows
+            // this lane's 16-byte chunk (4 tf32) and 8-byte half chunk (4 bf16) of its node's four rows
+            unsigned row_off[4], row_off16[4];
 #pragma unroll
-            for (int d = 0; d < 4; ++d) row_off[d] = (unsigned)sw128_chunk(nl_cur * 4 + d, j, S::B_ATOM);
+            for (int d = 0; d < 4; ++d) {
+                row_off[d] = (unsigned)sw128_chunk(nl_cur * 4 + d, j, S::B_ATOM);
+                row_off16[d] = (unsigned)sw128_chunk(nl_cur * 4 + d, j >> 1, S::B_ATOM) + (j & 1) * 8;
+            }
             const long long r_cur = r;
             const int c_cur = c;
             const bool valid_cur = valid;
@@ -640,7 +730,10 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
             for (int hh = 0; hh < 2; ++hh) {
                 const long long qq = 2 * i_cur + hh;
                 const int slot = (int)(qq % S::NSLOT);
-                bar_wait<CG, 64>(&empty[slot], (unsigned)(((qq / S::NSLOT) & 1) ^ 1));
+                const long long use = qq / S::NSLOT;           // this is the use-th fill of the slot
+                if (use > 0)                                   // wait for the MMAs of fill use - 1
+                    bar_wait<CG, 64>(&empty[slot + S::NSLOT * (int)((use - 1) & 1)],
+                                     (unsigned)(((use - 1) >> 1) & 1));
                 if (pw_cur == 0) TC_TRACE(i_cur, 9 + 2 * hh);
                 const unsigned slot_u = sB_u + slot * S::SLOT_BYTES;
                 const float4 cs4 = *reinterpret_cast<const float4 *>(csum + hh * S::KH + 4 * j);
@@ -655,9 +748,14 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
                     // normaliser partial sums (two lanes of a packed accumulator per direction)
                     fma2v(sd[d][0], sd[d][1], cs4.x, cs4.y, hv[0], hv[1]);
                     fma2v(sd[d][0], sd[d][1], cs4.z, cs4.w, hv[2], hv[3]);
-                    const unsigned o = slot_u + row_off[d];
-                    sts128(o, hi[0], hi[1], hi[2], hi[3]);
-                    sts128(o + S::B_PLANE, lo[0], lo[1], lo[2], lo[3]);
+                    sts128(slot_u + row_off[d], hi[0], hi[1], hi[2], hi[3]);
+                    if constexpr (C16) {
+                        const unsigned o16 = slot_u + S::B_PLANE + row_off16[d];
+                        sts64(o16, pack_bf16(hv[0], hv[1]), pack_bf16(hv[2], hv[3]));
+                        sts64(o16 + S::B_PLANE16, pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+                    } else {
+                        sts128(slot_u + S::B_PLANE + row_off[d], lo[0], lo[1], lo[2], lo[3]);
+                    }
                 }
                 if (hh == 1) {
                     // 1/s of the node's four messages, before the slot is published
@@ -705,9 +803,9 @@ __global__ void __launch_bounds__(TcShape<MS>::THREADS, 1) dense_tc_kernel(const
     }
 }
 
-template <int MS>
+template <int MS, bool C16>
 cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
-    using S = TcShape<MS>;
+    using S = TcShape<MS, C16>;
     static int clusters_max = 0;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
@@ -721,7 +819,7 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
     cfg.dynamicSmemBytes = S::SMEM;
     cfg.stream = s;
     if (!clusters_max) {
-        cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel<MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(dense_tc_kernel<MS, C16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)S::SMEM);
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0;
@@ -731,7 +829,7 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
         if (S::CG > 1) {
             cfg.gridDim = dim3(sms);
             int n = 0;
-            e = cudaOccupancyMaxActiveClusters(&n, dense_tc_kernel<MS>, &cfg);
+            e = cudaOccupancyMaxActiveClusters(&n, dense_tc_kernel<MS, C16>, &cfg);
             if (e != cudaSuccess) return e;
             if (n < 1) return cudaErrorLaunchOutOfResources;
             if (n < clusters_max) clusters_max = n;
@@ -744,7 +842,7 @@ cudaError_t launch_dense_tc_ms(const DenseArgs &a, cudaStream_t s) {
     if (clusters > clusters_max) clusters = clusters_max;
     if (launch_block_cap() > 0 && clusters > launch_block_cap()) clusters = launch_block_cap();
     cfg.gridDim = dim3((unsigned)(clusters * S::CG));
-    return cudaLaunchKernelEx(&cfg, dense_tc_kernel<MS>, a);
+    return cudaLaunchKernelEx(&cfg, dense_tc_kernel<MS, C16>, a);
 }
 
 }  // namespace tc
@@ -762,10 +860,10 @@ extern "C" __attribute__((visibility("default"))) int sbp_debug_tc_trace(long lo
 namespace sbp {
 #endif
 
-cudaError_t launch_dense_tc(const DenseArgs &a, cudaStream_t s) {
+cudaError_t launch_dense_tc(const DenseArgs &a, bool bf16_corrections, cudaStream_t s) {
     switch (a.Ms) {
-    case 128: return tc::launch_dense_tc_ms<128>(a, s);
-    case 256: return tc::launch_dense_tc_ms<256>(a, s);
+    case 128: return bf16_corrections ? tc::launch_dense_tc_ms<128, true>(a, s) : tc::launch_dense_tc_ms<128, false>(a, s);
+    case 256: return bf16_corrections ? tc::launch_dense_tc_ms<256, true>(a, s) : tc::launch_dense_tc_ms<256, false>(a, s);
     default: return cudaErrorNotSupported;
     }
 }

@@ -4,6 +4,9 @@
 //   mode 1  cta_group::1, A from tensor memory (lane = row, column = k), B smem
 //   mode 2  cta_group::2 (CTA pair, M = 256), A and B from shared memory
 //   mode 3  cta_group::2, A from tensor memory
+//   mode 4/5  kind::tf32 and kind::f16 (bf16, A packed two per tensor-memory column)
+//           products accumulated into one accumulator, cta_group::1 / ::2
+//   mode 9  MMA issue rate against N, SS / TS, cta_group
 // D[M x N] = A[M x K] * B[N x K]^T in kind::tf32, compared on the host with an
 // f64 product of the tf32-truncated inputs.
 //
@@ -247,6 +250,167 @@ static int run(const char *name) {
 }
 
 
+// ---- mode 4 / 5: kind::f16 (bf16 operands) with A from tensor memory, packed two
+// K-elements per 32-bit column, B from shared memory (K-major, 128-byte swizzle:
+// 64 bf16 per row), accumulated onto a kind::tf32 product in the same
+// accumulator: D = A32 * B32^T (tf32) + A16 * B16^T (bf16).
+#include <cuda_bf16.h>
+template <int CG>
+__device__ __forceinline__ void mma_ts_bf16(unsigned d, unsigned a_tmem, unsigned long long b, unsigned idesc, unsigned acc) {
+    if (CG == 1)
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc) : "memory");
+    else
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc) : "memory");
+}
+
+template <int CG>
+__global__ void __launch_bounds__(128) probe_mixed(const float *A32, const float *B32, const float *A16f, const float *B16f,
+                                                   float *D, int *status) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ unsigned tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    unsigned rank = 0;
+    if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    constexpr int NB = N / CG;
+    constexpr int B_ATOM = NB * 128;
+    unsigned char *sB32 = smem;                            // K/32 atoms
+    unsigned char *sB16 = smem + (K / 32) * B_ATOM;        // K/64 atoms
+    const float *Br32 = B32 + (size_t)rank * NB * K, *Br16 = B16f + (size_t)rank * NB * K;
+    for (int i = tid; i < NB * K; i += 128)
+        *(float *)(sB32 + sw128_off(i / K, i % K, B_ATOM)) = Br32[i];
+    for (int i = tid; i < NB * K; i += 128) {
+        const int row = i / K, k = i % K;                  // bf16: 8 elements per 16-byte chunk, 64 per atom
+        const int ka = k >> 6, c = (k & 63) >> 3;
+        const unsigned off = ka * B_ATOM + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4) + (k & 7) * 2;
+        *(__nv_bfloat16 *)(sB16 + off) = __float2bfloat16(Br16[i]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 0) {
+        if (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(512) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)), "n"(512) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = tmem_base_s;
+    {
+        // A32: lane = row, column 128 + k.  A16: column 256 + k / 2 holds (k even: low half, k odd: high half)
+        const float *a32 = A32 + ((size_t)rank * 128 + 32 * warp + lane) * K;
+        const float *a16 = A16f + ((size_t)rank * 128 + 32 * warp + lane) * K;
+        for (int k0 = 0; k0 < K; k0 += 32) {
+            float v[32];
+            for (int i = 0; i < 32; ++i) v[i] = a32[k0 + i];
+            tmem_st32(tmem + ((unsigned)(32 * warp) << 16) + 128 + k0, v);
+        }
+        for (int k0 = 0; k0 < K; k0 += 64) {
+            float v[32];
+            for (int i = 0; i < 32; ++i) {
+                __nv_bfloat162 p2 = __floats2bfloat162_rn(a16[k0 + 2 * i], a16[k0 + 2 * i + 1]);
+                v[i] = __uint_as_float(*reinterpret_cast<unsigned *>(&p2));
+            }
+            tmem_st32(tmem + ((unsigned)(32 * warp) << 16) + 256 + k0 / 2, v);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (CG == 2) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (tid == 0 && rank == 0) {
+        const unsigned mn = ((unsigned)(N >> 3) << 17) | ((unsigned)((128 * CG) >> 4) << 24);
+        const unsigned idesc32 = (1u << 4) | (2u << 7) | (2u << 10) | mn;
+        const unsigned idesc16 = (1u << 4) | (1u << 7) | (1u << 10) | mn;      // bf16 x bf16 -> f32
+        for (int k = 0; k < K / 8; ++k)
+            mma_ts<CG>(tmem, tmem + 128 + 8 * k, sw128_desc(smem_u32(sB32) + (k >> 2) * B_ATOM + (k & 3) * 32), idesc32, k > 0);
+        for (int k = 0; k < K / 16; ++k)
+            mma_ts_bf16<CG>(tmem, tmem + 256 + 8 * k, sw128_desc(smem_u32(sB16) + (k >> 2) * B_ATOM + (k & 3) * 32), idesc16, 1u);
+        if (CG == 1)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&bar)), "h"((unsigned short)3) : "memory");
+    }
+    const bool ok = mbar_wait(&bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (!ok) {
+        if (tid == 0) status[rank] = 1;
+    } else {
+        float v[32];
+        tmem_ld32(tmem + ((unsigned)(32 * warp) << 16), v);
+        for (int j = 0; j < N; ++j) D[((size_t)rank * 128 + 32 * warp + lane) * N + j] = v[j];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (CG == 2) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (warp == 0) {
+        if (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+    }
+}
+
+static float bf16_round(float x) { return __bfloat162float(__float2bfloat16(x)); }
+
+template <int CG>
+static int run_mixed(const char *name) {
+    const int M = 128 * CG;
+    std::vector<float> A32((size_t)M * K), B32((size_t)N * K), A16((size_t)M * K), B16((size_t)N * K), D((size_t)M * N, -1.0f);
+    srand(4321);
+    for (auto &x : A32) x = tf32_trunc((float)rand() / RAND_MAX + 0.01f);
+    for (auto &x : B32) x = tf32_trunc((float)rand() / RAND_MAX - 0.3f);
+    for (auto &x : A16) x = bf16_round((float)rand() / RAND_MAX - 0.5f);
+    for (auto &x : B16) x = bf16_round((float)rand() / RAND_MAX + 0.2f);
+    float *d[5]; int *dS, hS[2] = {0, 0};
+    std::vector<float> *h[4] = {&A32, &B32, &A16, &B16};
+    for (int i = 0; i < 4; ++i) { CK(cudaMalloc(&d[i], h[i]->size() * 4)); CK(cudaMemcpy(d[i], h[i]->data(), h[i]->size() * 4, cudaMemcpyHostToDevice)); }
+    CK(cudaMalloc(&d[4], D.size() * 4)); CK(cudaMemcpy(d[4], D.data(), D.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&dS, 8)); CK(cudaMemset(dS, 0, 8));
+    const size_t smem = (K / 32) * (N / CG * 128) + (K / 64) * (N / CG * 128);
+    CK(cudaFuncSetAttribute(probe_mixed<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CG); cfg.blockDim = dim3(128); cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, probe_mixed<CG>, (const float *)d[0], (const float *)d[1], (const float *)d[2], (const float *)d[3], d[4], dS));
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("%s: kernel failed: %s\n", name, cudaGetErrorString(e)); return 2; }
+    CK(cudaMemcpy(D.data(), d[4], D.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hS, dS, 8, cudaMemcpyDeviceToHost));
+    double worst = 0.0; int bad = 0;
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) {
+            double ref = 0.0;
+            for (int k = 0; k < K; ++k)
+                ref += (double)A32[(size_t)i * K + k] * B32[(size_t)j * K + k] + (double)A16[(size_t)i * K + k] * B16[(size_t)j * K + k];
+            const double err = fabs(ref - D[(size_t)i * N + j]) / (fabs(ref) + 1.0);
+            if (err > worst) worst = err;
+            if (err > 1e-4) ++bad;
+        }
+    printf("%s: timeout flags %d %d, worst rel err %.3e, bad %d of %d\n", name, hS[0], hS[1], worst, bad, M * N);
+    return bad || hS[0] || hS[1];
+}
+
 // ---- MMA issue-rate benchmark: REP back-to-back tcgen05.mma (kind::tf32, K = 8)
 // of shape (128 CG) x NN, A from shared memory (SS) or tensor memory (TS);
 // cycles per MMA from clock64 around issue + commit + wait.
@@ -345,6 +509,8 @@ int main(int argc, char **argv) {
     if (mode < 0 || mode == 1) rc |= run<1, true>("mode1 cg1 TS");
     if (mode < 0 || mode == 2) rc |= run<2, false>("mode2 cg2 SS");
     if (mode < 0 || mode == 3) rc |= run<2, true>("mode3 cg2 TS");
+    if (mode < 0 || mode == 4) rc |= run_mixed<1>("mode4 cg1 tf32 TS + bf16 TS, one accumulator");
+    if (mode < 0 || mode == 5) rc |= run_mixed<2>("mode5 cg2 tf32 TS + bf16 TS, one accumulator");
     if (mode == 9) {
         rate<1, false, 32>("cg1 SS"); rate<1, false, 64>("cg1 SS"); rate<1, false, 128>("cg1 SS"); rate<1, false, 256>("cg1 SS");
         rate<1, true, 32>("cg1 TS"); rate<1, true, 64>("cg1 TS"); rate<1, true, 128>("cg1 TS"); rate<1, true, 256>("cg1 TS");
