@@ -156,12 +156,29 @@ __device__ __forceinline__ float lanes_sum(float v) {
     return v;
 }
 
-template <int LP>
+// RX: the warp-wide float max of sm_100a in one instruction (redux.sync.max.f32,
+// SASS CREDUX.MAX.F32; NaN operands are ignored like fmaxf) instead of five
+// SHFL + FMNMX steps.  Same value, so same bits; opt-in per kernel (it wins
+// for the max-sum tap kernels at R <= 16: C5 T=9 2.05 -> 1.92 ms, T=17 2.78 ->
+// 2.65, and loses 2 % in the one-copy R = 32 body; profiles/r02_ab_redux.txt).
+template <int LP, bool RX = false>
 __device__ __forceinline__ float lanes_max(float v) {
+    if (RX && LP == 32) {
+        float r;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+        return r;
+    }
 #pragma unroll
     for (int off = 1; off < LP; off <<= 1) v = fmaxf(v, __shfl_xor_sync(SBP_FULL_MASK, v, off));
     return v;
 }
+
+// Kernels whose warp-wide maxima use redux.sync (lanes_max RX): max-sum, one
+// node per warp (Ms = 256), 4 <= R <= 16 -- measured per C5 band: T=5 1.86 ->
+// 1.61 ms, T=9 2.05 -> 1.92, T=17 2.78 -> 2.65; slower for R = 1 (T=2: 1.55 ->
+// 1.68) and in the one-copy R = 32 body (profiles/r02_ab_redux.txt).
+template <int DOM, int LP, int R>
+constexpr bool band_redux() { return DOM == SBP_MAX && LP == 32 && R >= 4 && R <= 16; }
 
 // h value at lane-relative label offset t (t in [-R, VL+R)).
 template <int DOM, int VL, int LP, int R>
@@ -261,7 +278,7 @@ __device__ __forceinline__ void two_sum(float a, float b, float &s, float &e) {
 
 // h'[i] = (s[i] - c) + e[i] with c = max over the node's labels of s.
 // Pairs of labels use the packed FP32 ops (bit-identical to the scalar ones).
-template <int VL, int LP>
+template <int VL, int LP, bool RX = false>
 __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const float (&e)[VL],
                                                   float (&h)[VL]) {
     float c = s[0];
@@ -270,7 +287,7 @@ __device__ __forceinline__ void shift_compensated(const float (&s)[VL], const fl
 #pragma unroll
     for (int i = i0; i + 1 < VL; i += 2) c = fmax3(c, s[i], s[i + 1]);
     if ((VL - i0) % 2 == 1) c = fmaxf(c, s[VL - 1]);
-    c = lanes_max<LP>(c);
+    c = lanes_max<LP, RX>(c);
     if (!isfinite(c)) c = 0.0f;
 #pragma unroll
     for (int i = 0; i + 1 < VL; i += 2) {
@@ -353,7 +370,7 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
         float mx = fmaxf(h[0], h[1]);
 #pragma unroll
         for (int i = 2; i < VL; i += 2) mx = fmax3(mx, h[i], h[i + 1]);
-        mx = lanes_max<LP>(mx);
+        mx = lanes_max<LP, band_redux<DOM, LP, R>()>(mx);
         const float base = a.floor_term ? a.fbar[O] + mx : -__builtin_huge_valf();
 #pragma unroll
         for (int i = 0; i < VL; ++i) out[i] = base;
@@ -425,7 +442,7 @@ __device__ __forceinline__ bool band_message(const BandArgs &a, const float (&h)
         float mx = fmaxf(out[0], out[1]);
 #pragma unroll
         for (int i = 2; i < VL; i += 2) mx = fmax3(mx, out[i], out[i + 1]);
-        mx = lanes_max<LP>(mx);
+        mx = lanes_max<LP, band_redux<DOM, LP, R>()>(mx);
         ok = isfinite(mx);
 #pragma unroll
         for (int i = 0; i < VL; i += 2) sub2(out[i], out[i + 1], out[i], out[i + 1], mx, mx);
@@ -502,24 +519,24 @@ __device__ __forceinline__ void band_group_body(const BandArgs &a, const IterCtx
             vtwo_sum(g, m1, s2, e2);
             vtwo_sum_acc(s2, m2, e2, e2);
             vtwo_sum_acc(s2, m3, e2, e2);
-            shift_compensated<VL, LP>(s2, e2, h);
+            shift_compensated<VL, LP, band_redux<DOM, LP, R>()>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(3)>(a, it, h, 3, j, x0, valid && has_u, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_l)) {                     // excl 1
             vtwo_sum_from(sa, ea, m2, s2, e2);
             vtwo_sum_acc(s2, m3, e2, e2);
-            shift_compensated<VL, LP>(s2, e2, h);
+            shift_compensated<VL, LP, band_redux<DOM, LP, R>()>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(1)>(a, it, h, 1, j, x0, valid && has_l, node_l, r, c);
         }
         vtwo_sum_acc(sa, m1, ea, ea);                                        // g + m0 + m1
         if (__any_sync(SBP_FULL_MASK, valid && has_r)) {                     // excl 2
             vtwo_sum_from(sa, ea, m3, s2, e2);
-            shift_compensated<VL, LP>(s2, e2, h);
+            shift_compensated<VL, LP, band_redux<DOM, LP, R>()>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(0)>(a, it, h, 0, j, x0, valid && has_r, node_l, r, c);
         }
         if (__any_sync(SBP_FULL_MASK, valid && has_d)) {                     // excl 3
             vtwo_sum_from(sa, ea, m2, s2, e2);
-            shift_compensated<VL, LP>(s2, e2, h);
+            shift_compensated<VL, LP, band_redux<DOM, LP, R>()>(s2, e2, h);
             emit_direction<DOM, VL, LP, R, dir_orient(2)>(a, it, h, 2, j, x0, valid && has_d, node_l, r, c);
         }
     }
@@ -671,7 +688,7 @@ __device__ __forceinline__ void band_group_body_rolled(const BandArgs &a, const 
             } else {
                 vtwo_sum_from(pb, eb, m2, s2, e2);
             }
-            shift_compensated<VL, LP>(s2, e2, h);
+            shift_compensated<VL, LP, band_redux<DOM, LP, R>()>(s2, e2, h);
         }
         emit_direction<DOM, VL, LP, R, 0>(a, it, h, dir, j, x0, valid && hd, node_l, r, c);
     }

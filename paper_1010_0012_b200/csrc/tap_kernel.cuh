@@ -444,14 +444,18 @@ cudaError_t launch_band_tap(const BandArgs &a, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 
 // Sum (S) or max (H) of a lane's h over the node, as band_message forms it.
-template <int DOM, int VL, int LP>
+template <int DOM, int VL, int LP, bool RX = false>
 __device__ __forceinline__ float node_reduce(const float (&h)[VL]) {
     if (DOM == SBP_SUM) return lanes_sum<LP>(vsum(h));
     float mx = fmaxf(h[0], h[1]);
 #pragma unroll
     for (int i = 2; i < VL; i += 2) mx = fmax3(mx, h[i], h[i + 1]);
-    return lanes_max<LP>(mx);
+    return lanes_max<LP, RX>(mx);
 }
+
+// The v2 kernels reduce maxima with redux.sync (lanes_max) where it measured faster.
+template <int DOM, int LP, int R>
+constexpr bool tap2_redux() { return band_redux<DOM, LP, R>(); }
 
 template <int DOM, int VL, int LP>
 __device__ __forceinline__ void put_row(float *row, int x0, const float (&h)[VL]) {
@@ -532,7 +536,7 @@ __device__ __forceinline__ bool tap2_message(const BandArgs &a, float red, int x
         float mx = fmaxf(out[0], out[1]);
 #pragma unroll
         for (int i = 2; i < VL; i += 2) mx = fmax3(mx, out[i], out[i + 1]);
-        mx = lanes_max<LP>(mx);
+        mx = lanes_max<LP, tap2_redux<DOM, LP, R>()>(mx);
         ok = isfinite(mx);
 #pragma unroll
         for (int i = 0; i < VL; i += 2) sub2(out[i], out[i + 1], out[i], out[i + 1], mx, mx);
@@ -559,7 +563,7 @@ __device__ __forceinline__ void tap2_emit(const BandArgs &a, const IterCtx &it, 
 }
 
 // Rows of a node: rows[dir] holds h_{i \ dir's target}; red[dir] its S / H.
-template <int DOM, int VL, int LP>
+template <int DOM, int VL, int LP, bool RX>
 __device__ __forceinline__ void tap2_form_h(const float (&g)[VL], const float (&m0)[VL],
                                             const float (&m1)[VL], const float (&m2)[VL],
                                             const float (&m3)[VL], int x0, float *rows,
@@ -573,44 +577,44 @@ __device__ __forceinline__ void tap2_form_h(const float (&g)[VL], const float (&
         vmul(h, h, m2);
         vmul(h, h, m3);                               // excl 0 -> dir 3
         put_row<DOM, VL, LP>(rows + 3 * ROWF, x0, h);
-        red[3] = node_reduce<DOM, VL, LP>(h);
+        red[3] = node_reduce<DOM, VL, LP, RX>(h);
         float ab[VL];
         vmul(ab, g, m0);
         vmul(h, ab, m2);
         vmul(h, h, m3);                               // excl 1 -> dir 1
         put_row<DOM, VL, LP>(rows + 1 * ROWF, x0, h);
-        red[1] = node_reduce<DOM, VL, LP>(h);
+        red[1] = node_reduce<DOM, VL, LP, RX>(h);
         vmul(ab, ab, m1);
         vmul(h, ab, m3);                              // excl 2 -> dir 0
         put_row<DOM, VL, LP>(rows + 0 * ROWF, x0, h);
-        red[0] = node_reduce<DOM, VL, LP>(h);
+        red[0] = node_reduce<DOM, VL, LP, RX>(h);
         vmul(h, ab, m2);                              // excl 3 -> dir 2
         put_row<DOM, VL, LP>(rows + 2 * ROWF, x0, h);
-        red[2] = node_reduce<DOM, VL, LP>(h);
+        red[2] = node_reduce<DOM, VL, LP, RX>(h);
     } else {
         float s2[VL], e2[VL];
         vtwo_sum(g, m1, s2, e2);
         vtwo_sum_acc(s2, m2, e2, e2);
         vtwo_sum_acc(s2, m3, e2, e2);
-        shift_compensated<VL, LP>(s2, e2, h);        // excl 0 -> dir 3
+        shift_compensated<VL, LP, RX>(s2, e2, h);        // excl 0 -> dir 3
         put_row<DOM, VL, LP>(rows + 3 * ROWF, x0, h);
-        red[3] = node_reduce<DOM, VL, LP>(h);
+        red[3] = node_reduce<DOM, VL, LP, RX>(h);
         float sa[VL], ea[VL];
         vtwo_sum(g, m0, sa, ea);
         vtwo_sum_from(sa, ea, m2, s2, e2);
         vtwo_sum_acc(s2, m3, e2, e2);
-        shift_compensated<VL, LP>(s2, e2, h);        // excl 1 -> dir 1
+        shift_compensated<VL, LP, RX>(s2, e2, h);        // excl 1 -> dir 1
         put_row<DOM, VL, LP>(rows + 1 * ROWF, x0, h);
-        red[1] = node_reduce<DOM, VL, LP>(h);
+        red[1] = node_reduce<DOM, VL, LP, RX>(h);
         vtwo_sum_acc(sa, m1, ea, ea);
         vtwo_sum_from(sa, ea, m3, s2, e2);
-        shift_compensated<VL, LP>(s2, e2, h);        // excl 2 -> dir 0
+        shift_compensated<VL, LP, RX>(s2, e2, h);        // excl 2 -> dir 0
         put_row<DOM, VL, LP>(rows + 0 * ROWF, x0, h);
-        red[0] = node_reduce<DOM, VL, LP>(h);
+        red[0] = node_reduce<DOM, VL, LP, RX>(h);
         vtwo_sum_from(sa, ea, m2, s2, e2);
-        shift_compensated<VL, LP>(s2, e2, h);        // excl 3 -> dir 2
+        shift_compensated<VL, LP, RX>(s2, e2, h);        // excl 3 -> dir 2
         put_row<DOM, VL, LP>(rows + 2 * ROWF, x0, h);
-        red[2] = node_reduce<DOM, VL, LP>(h);
+        red[2] = node_reduce<DOM, VL, LP, RX>(h);
     }
 }
 
@@ -791,7 +795,7 @@ band_iter_tap2_kernel(const __grid_constant__ BandArgs a) {
                 }
             }
             __syncwarp();   // the previous group's messages are done reading the rows
-            tap2_form_h<DOM, VL, LP>(g, m0, m1, m2, m3, x0, rows, red);
+            tap2_form_h<DOM, VL, LP, tap2_redux<DOM, LP, R>()>(g, m0, m1, m2, m3, x0, rows, red);
             if constexpr (STG == 3) {
                 if (grp + nwarps < ngroups) load_regs(grp + nwarps);
             }

@@ -95,6 +95,12 @@ def test_integration_stub_runs_verbatim(monkeypatch):
     torch.testing.assert_close(got[:, 1:-1], want[:, 1:-1], rtol=0, atol=0)
     got_f = ns["run_grid_gpu_fused"](model, 9, [w0, w1], pot.fbar, R)
     torch.testing.assert_close(got_f[:, 1:-1], want[:, 1:-1], rtol=0, atol=0)
+    # the dense binding (tensor cores at M = 128): same bits as kernel="standard"
+    m128 = synth.build_config_model(synth.CONFIGS["C4"], height=9, width=14)
+    want_d = sbp.run_sweeps(m128, 4, kernel="standard", schedule="synchronous").engine
+    assert want_d.kernel_name.startswith("dense_tc_kernel")
+    got_d = ns["run_grid_gpu_dense"](m128, 4, m128.shared_potential.densify().table)
+    torch.testing.assert_close(got_d[:, 1:-1], want_d.current[:, 1:-1], rtol=0, atol=0)
 
 
 @pytest.mark.parametrize("schedule", ["synchronous", None])
