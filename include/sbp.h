@@ -100,7 +100,8 @@ typedef struct {
                                              m_max = M, idx[k][x] = k.  A symmetric table may
                                              pass the SAME pointer twice: sum-product at
                                              Ms = 128 / 256 then runs as a 3xTF32 GEMM on the
-                                             tensor cores (tcgen05; SBP_DENSE_TC=0: SIMT) */
+                                             tensor cores (tcgen05; SBP_DENSE_TC=0: SIMT,
+                                             2: bf16 correction products, faster, 5.7e-6) */
     /* ELL per-edge (inhomogeneous) potentials, n_pot > 0: ell_idx[0] / ell_w[0]
      * point at [n_pot][2][m_max][Ms], fbar_all at [n_pot][2]; pid_h[r*W + c]
      * is the potential of edge (n, n+1), pid_v[r*W + c] of edge (n, n+W)
