@@ -52,25 +52,39 @@ def max_dev(a, b):
 _engines: dict = {}
 
 
-def _engine(cfg_name, domain, schedule):
-    """One engine per (config, domain, schedule); the unary table is built on
-    the host in f64 by the reference formula (stereo.py:82-99) and loaded."""
-    key = (cfg_name, domain, schedule)
+def _engine(cfg_name, domain, schedule, kernel="fast"):
+    """One engine per (config, domain, schedule, kernel); the unary table is
+    built on the host in f64 by the reference formula (stereo.py:82-99) and loaded."""
+    key = (cfg_name, domain, schedule, kernel)
     if key not in _engines:
         _engines.clear()
         torch.cuda.empty_cache()
         cfg = synth.CONFIGS[cfg_name]
-        _engines[key] = GridEngine(synth.StripModel(cfg), domain, "fast",
+        _engines[key] = GridEngine(synth.StripModel(cfg), domain, kernel,
                                    values=synth.config_values(cfg, domain), schedule=schedule)
     return _engines[key]
 
 
 @pytest.mark.parametrize("name", sorted(MAN["cases"]))
 def test_full_size_against_reference(name):
+    _check_case(name, "fast")
+
+
+@pytest.mark.parametrize("name", [n for n in ("C4_sync_sum", "C5_T9_sync_sum", "C5_T33_sync_sum")
+                                  if n in MAN["cases"]])
+def test_full_size_tensor_core_dense(name):
+    """kernel="standard" at full size: the dense update on the tensor cores
+    (3xTF32) against the same reference fixtures -- the O(M^2) and the O(mM)
+    updates are the same function (numba_kernels.py:35-54)."""
+    eng = _check_case(name, "standard")
+    assert eng.kernel_name.startswith("dense_tc_kernel"), eng.kernel_name
+
+
+def _check_case(name, kernel):
     e = MAN["cases"][name]
     z = np.load(FULL / f"{name}.npz")
     dom = e["domain"]
-    eng = _engine(e["config"], dom, SEQUENTIAL if e["schedule"] == "seq" else SYNCHRONOUS)
+    eng = _engine(e["config"], dom, SEQUENTIAL if e["schedule"] == "seq" else SYNCHRONOUS, kernel)
     eng.reset()
     eng.step(e["iters"])
     torch.cuda.synchronize()
@@ -108,3 +122,4 @@ def test_full_size_against_reference(name):
     else:
         assert max_dev(got, want) <= MAX_TOL
         assert max_dev(gb, z["sample_scores"]) <= MAX_TOL
+    return eng
