@@ -62,12 +62,19 @@ class FakeDist:
         return reqs
 
 
-@pytest.mark.parametrize("world,domain", [(2, "sum"), (3, "max")])
-def test_threaded_ranks_match_whole_grid(world, domain):
-    cfg = synth.CONFIGS["C2"]
+@pytest.mark.parametrize("world,domain,cfg_name,kernel", [
+    (2, "sum", "C2", "fast"), (3, "max", "C2", "fast"),
+    # kernel="standard" on the tensor cores: row sub-ranges with halo rows, the
+    # boundary and interior launches on two streams (each allocates tensor memory)
+    (2, "sum", "C4", "standard"), (3, "sum", "C5_T9", "standard")])
+def test_threaded_ranks_match_whole_grid(world, domain, cfg_name, kernel):
+    cfg = synth.CONFIGS[cfg_name]
     H, W, iters = 29, 48, 7
     model = synth.build_config_model(cfg, height=H, width=W)
-    full = sbp.run_sweeps(model, iters, domain=domain, schedule="synchronous").engine.msgs4()
+    whole = sbp.run_sweeps(model, iters, kernel=kernel, domain=domain, schedule="synchronous")
+    if kernel == "standard":
+        assert whole.engine.kernel_name.startswith("dense_tc_kernel")
+    full = whole.engine.msgs4()
     fake = FakeDist()
     parts = [None] * world
     splits = [None] * world
@@ -77,7 +84,7 @@ def test_threaded_ranks_match_whole_grid(world, domain):
         threading.current_thread().rank = rank
         try:
             r0, rows = partition_rows(H, world)[rank]
-            strip = GpuStrip(model, r0, rows, domain, "fast")
+            strip = GpuStrip(model, r0, rows, domain, kernel)
             interior = torch.cuda.Stream()
             timing = []
             with torch.cuda.stream(torch.cuda.Stream()):
