@@ -738,8 +738,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 // NS = 2: double buffer, the next group's copy is issued before waiting for
 // the current one.  NS = 1: one buffer, the next copy is issued as soon as the
 // current group has moved to registers (half the shared memory, for VL = 16).
+// Staged VL = 16 kernel (sum, Ms >= 128): 4 resident blocks per SM (124
+// registers, no spills) instead of the 3 its 136 registers allowed: C5 T=5 sum
+// 1.565 vs 1.595 ms per iteration, cold and sustained
+// (profiles/r02_ab_staged16_blocks.txt).  0: no register bound.
+#ifndef SBP_STG16_BLOCKS
+#define SBP_STG16_BLOCKS 4
+#endif
 template <int DOM, int VL, int LP, int R, int NS>
-__global__ void __launch_bounds__(32 * STG_WARPS)
+__global__ void __launch_bounds__(32 * STG_WARPS, (VL == 16 && SBP_STG16_BLOCKS > 0 ? SBP_STG16_BLOCKS : 1))
 band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
     float dmax = 0.0f;

@@ -296,13 +296,14 @@ __device__ __forceinline__ void tap_rows_init(float *rows) {
 
 // NS = 0: register-loaded inputs (256-bit LDG); NS = 1 / 2: TMA-staged inputs
 // (one / two stages of 1-D bulk copies per warp, as band_iter_staged_kernel).
-// Resident blocks per SM.  VL = 16 at Ms = 128 (C4): 4 blocks (128 registers,
-// no spills) instead of 3 (146 registers) -- slower cold (2.49 vs 2.26 ms) but
-// faster where the benchmark and any run longer than the power-cap response
-// live: sustained 2.38 vs 2.48 ms per iteration at ~990 W (0.93 vs 0.89 of the
-// copy peak; profiles/r02_ab_c4_tap_blocks.txt).  SBP_TAP16_BLOCKS overrides.
+// Resident blocks per SM.  VL = 16: 4 blocks (126-128 registers, no spills)
+// instead of 3 (146 registers) -- slower cold (C4 2.49 vs 2.26 ms, C5 T=9 1.60
+// vs 1.52) but faster where the benchmark and any workload longer than the
+// power-cap response live: sustained at ~990 W C4 2.38 vs 2.48 ms per iteration
+// (0.93 vs 0.89 of the copy peak), C5 T=9 1.57 vs 1.65 (0.94 vs 0.89;
+// profiles/r02_ab_c4_tap_blocks.txt, r02_ab_t9_tap_blocks.txt).
 #ifndef SBP_TAP16_BLOCKS
-#define SBP_TAP16_BLOCKS(MS) ((MS) == 128 ? 4 : 3)
+#define SBP_TAP16_BLOCKS(MS) 4
 #endif
 template <int DOM, int VL, int LP, int R, bool ROLLED, int NS>
 __global__ void __launch_bounds__(32 * TAP_WARPS, (VL == 8 ? 4 : SBP_TAP16_BLOCKS(VL * LP)))
