@@ -746,7 +746,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 #define SBP_STG16_BLOCKS 4
 #endif
 template <int DOM, int VL, int LP, int R, int NS>
-__global__ void __launch_bounds__(32 * STG_WARPS, (VL == 16 && SBP_STG16_BLOCKS > 0 ? SBP_STG16_BLOCKS : 1))
+__global__ void __launch_bounds__(32 * STG_WARPS, (VL == 16 ? SBP_STG16_BLOCKS : 0))
 band_iter_staged_kernel(const __grid_constant__ BandArgs a) {
     constexpr int PPW = 32 / LP;
     float dmax = 0.0f;
